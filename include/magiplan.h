@@ -1,0 +1,190 @@
+/* magiplan C ABI — B200-native drop-in for the reference planner's C ABI
+ * (/root/reference/proj/include/magiplan/magiplan.h:43-121) plus the Flexible
+ * Flash Attention (FFA) and context-parallel entry points the reference only
+ * models as cost terms (proj/include/magiplan/overlap.hpp:44-50).
+ *
+ * Conventions (unchanged from the reference, magiplan.h:19-25):
+ *   - every function returns a magiplan_status; failures leave outputs
+ *     untouched and record a message readable via magiplan_last_error()
+ *     (thread-local); success clears it;
+ *   - strings returned through char** are heap-allocated; release them with
+ *     magiplan_string_free;
+ *   - handles are opaque; release them with the matching _free call.
+ * Added conventions for device entry points:
+ *   - tensors are caller-owned device pointers, passed as void* / float*;
+ *   - cuda_stream is a cudaStream_t passed as void* (NULL = legacy stream);
+ *   - launches are asynchronous on cuda_stream; no hidden device sync;
+ *   - CUDA failures map to MAGIPLAN_ERR_INTERNAL with the CUDA error text.
+ */
+#ifndef MAGIPLAN_H
+#define MAGIPLAN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define MAGIPLAN_API __declspec(dllexport)
+#else
+#define MAGIPLAN_API __attribute__((visibility("default")))
+#endif
+
+/* reference: magiplan.h:43-51 */
+typedef enum magiplan_status {
+  MAGIPLAN_OK = 0,
+  MAGIPLAN_ERR_USAGE = 2,
+  MAGIPLAN_ERR_CONSTRAINT = 3,
+  MAGIPLAN_ERR_INTERNAL = 4
+} magiplan_status;
+
+/* reference: magiplan.h:53-56 */
+typedef enum magiplan_counting {
+  MAGIPLAN_COUNT_MULTIPLICITY = 0,
+  MAGIPLAN_COUNT_UNION = 1
+} magiplan_counting;
+
+/* AttnSlice mask types; the values are the reference enum's
+ * (proj/include/magiplan/mask.hpp:52). */
+typedef enum magiplan_slice_type {
+  MAGIPLAN_SLICE_FULL = 0,
+  MAGIPLAN_SLICE_CAUSAL = 1,
+  MAGIPLAN_SLICE_INV_CAUSAL = 2,
+  MAGIPLAN_SLICE_BI_CAUSAL = 3
+} magiplan_slice_type;
+
+typedef enum magiplan_dtype { MAGIPLAN_F32 = 0, MAGIPLAN_BF16 = 1 } magiplan_dtype;
+
+typedef struct magiplan_mask magiplan_mask;
+typedef struct magiplan_scenario magiplan_scenario;
+typedef struct magiplan_ffa_plan magiplan_ffa_plan;
+
+/* ---- library ---------------------------------------------------------- */
+/* reference: magiplan.h:61-67, capi.cpp:74-78 */
+MAGIPLAN_API const char* magiplan_version(void);
+MAGIPLAN_API const char* magiplan_last_error(void);
+MAGIPLAN_API void magiplan_string_free(char* text);
+
+/* ---- attention masks (reference: magiplan.h:69-98) -------------------- */
+MAGIPLAN_API magiplan_status magiplan_mask_parse(const char* spec_json, magiplan_mask** out_mask);
+MAGIPLAN_API void magiplan_mask_free(magiplan_mask* mask);
+MAGIPLAN_API magiplan_status magiplan_mask_area(const magiplan_mask* mask,
+                                                magiplan_counting counting, int64_t* out_area);
+MAGIPLAN_API magiplan_status magiplan_mask_is_allowed(const magiplan_mask* mask, int64_t q,
+                                                      int64_t k, int* out_allowed);
+MAGIPLAN_API magiplan_status magiplan_mask_render(const magiplan_mask* mask, char** out_text);
+MAGIPLAN_API magiplan_status magiplan_mask_describe(const magiplan_mask* mask, char** out_json);
+
+/* ---- planning scenarios (reference: magiplan.h:100-118) --------------- */
+MAGIPLAN_API magiplan_status magiplan_scenario_parse(const char* scenario_json,
+                                                     const char* base_dir,
+                                                     magiplan_scenario** out_scenario);
+MAGIPLAN_API void magiplan_scenario_free(magiplan_scenario* scenario);
+MAGIPLAN_API magiplan_status magiplan_scenario_set_seed(magiplan_scenario* scenario,
+                                                        uint64_t seed);
+MAGIPLAN_API magiplan_status magiplan_scenario_plan(const magiplan_scenario* scenario,
+                                                    char** out_json);
+MAGIPLAN_API magiplan_status magiplan_scenario_simulate(const magiplan_scenario* scenario,
+                                                        int jobs, char** out_jsonl);
+MAGIPLAN_API magiplan_status magiplan_pack_run(const char* config_json, const char* stream_text,
+                                               char** out_json);
+
+/* ---- context-parallel execution plan (new) ----------------------------- */
+/* Executor view of magiplan_scenario_plan for the real multi-GPU run: per
+ * rank its query chunks, and per forward/backward stage the KV token ranges
+ * it receives (in receive-buffer order) together with the rank's local
+ * slices re-expressed against [local KV | stage receive buffer] coordinates.
+ * JSON object; see INTEGRATION.md for the field list. */
+MAGIPLAN_API magiplan_status magiplan_scenario_exec_plan(const magiplan_scenario* scenario,
+                                                         char** out_json);
+
+/* ---- Flexible Flash Attention (new; no reference counterpart beyond the
+ *      cost terms CostModel::ffa_fwd / ffa_bwd, overlap.hpp:47-48) ------- */
+
+/* Compile a slice list into the device work list consumed by the kernels.
+ * q_ranges / k_ranges: host int64 [num_slices][2] half-open ranges; types:
+ * host int32 [num_slices] magiplan_slice_type. head_dim in {64, 128}.
+ * Overlapping slices are legal and computed with MULTIPLICITY semantics
+ * (mask.hpp:85): a pair covered by m slices contributes m times. The plan
+ * owns device memory and is reusable across calls, heads and layers. */
+MAGIPLAN_API magiplan_status magiplan_ffa_plan_create(const int64_t* q_ranges,
+                                                      const int64_t* k_ranges,
+                                                      const int32_t* types, int64_t num_slices,
+                                                      int64_t seqlen_q, int64_t seqlen_k,
+                                                      int32_t head_dim,
+                                                      magiplan_ffa_plan** out_plan);
+MAGIPLAN_API magiplan_status magiplan_ffa_plan_from_mask(const magiplan_mask* mask,
+                                                         int32_t head_dim,
+                                                         magiplan_ffa_plan** out_plan);
+MAGIPLAN_API void magiplan_ffa_plan_free(magiplan_ffa_plan* plan);
+/* {"seqlen_q","seqlen_k","head_dim","num_slices","area_multiplicity",
+ *  "q_tiles","fwd_items","fwd_ktiles","bwd_items","bwd_qtiles"} */
+MAGIPLAN_API magiplan_status magiplan_ffa_plan_describe(const magiplan_ffa_plan* plan,
+                                                        char** out_json);
+
+/* Forward. q: [seqlen_q, num_heads_q, head_dim] bf16; k, v: [seqlen_k,
+ * num_heads_k, head_dim] bf16 (GQA: num_heads_q % num_heads_k == 0);
+ * out: [seqlen_q, num_heads_q, head_dim] in out_dtype; lse: [num_heads_q,
+ * seqlen_q] f32 (natural log; -inf for rows with no allowed key).
+ * accumulate != 0 merges this call into an existing (out, lse) pair with the
+ * log-sum-exp correction (requires out_dtype == MAGIPLAN_F32): this is the
+ * per-stage merge of the context-parallel forward. */
+MAGIPLAN_API magiplan_status magiplan_ffa_fwd(const magiplan_ffa_plan* plan, const void* q,
+                                              const void* k, const void* v, void* out,
+                                              float* lse, int64_t num_heads_q,
+                                              int64_t num_heads_k, float softmax_scale,
+                                              int32_t out_dtype, int32_t accumulate,
+                                              void* cuda_stream);
+
+/* delta[h, i] = sum_d out[i, h, d] * grad_out[i, h, d] (f32 [num_heads,
+ * seqlen]); out in out_dtype, grad_out bf16. */
+MAGIPLAN_API magiplan_status magiplan_ffa_bwd_preprocess(const void* out, const void* grad_out,
+                                                         float* delta, int64_t seqlen,
+                                                         int64_t num_heads, int32_t head_dim,
+                                                         int32_t out_dtype, void* cuda_stream);
+
+/* Backward: grad_q [seqlen_q, hq, d], grad_k / grad_v [seqlen_k, hk, d] in
+ * grad_dtype; accumulate != 0 adds into them (f32 only). Deterministic: no
+ * unordered atomics; every gradient element is produced by one CTA in a
+ * fixed order, so reruns are bitwise identical. */
+MAGIPLAN_API magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, const void* q,
+                                              const void* k, const void* v, const float* lse,
+                                              const float* delta, const void* grad_out,
+                                              void* grad_q, void* grad_k, void* grad_v,
+                                              int64_t num_heads_q, int64_t num_heads_k,
+                                              float softmax_scale, int32_t grad_dtype,
+                                              int32_t accumulate, void* cuda_stream);
+
+/* ---- context-parallel data movement kernels (new) ---------------------- */
+/* Gather token ranges of a [tokens, width] row-major buffer into a packed
+ * buffer (Range Gather). ranges: device int64 [n][2];
+ * offsets: device int64 [n] destination row of each range. */
+MAGIPLAN_API magiplan_status magiplan_range_gather(const void* src, void* dst,
+                                                   const int64_t* ranges, const int64_t* offsets,
+                                                   int64_t num_ranges, int64_t total_rows,
+                                                   int64_t row_bytes, void* cuda_stream);
+/* dst[ranges[i]] += src_packed[offsets[i] ...] in f32, ranges applied in
+ * index order (deterministic Range Scatter-Reduce). */
+MAGIPLAN_API magiplan_status magiplan_range_scatter_add_f32(const float* src, float* dst,
+                                                            const int64_t* ranges,
+                                                            const int64_t* offsets,
+                                                            int64_t num_ranges,
+                                                            int64_t total_rows,
+                                                            int64_t row_elems,
+                                                            void* cuda_stream);
+/* f32 -> bf16 conversion of n elements. */
+MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
+                                                    void* cuda_stream);
+
+/* ---- diagnostics ------------------------------------------------------- */
+/* One 128x128x128 bf16 tile product through the TMA/UMMA building blocks
+ * (C = A B^T for b_mn_major == 0, C = A B otherwise). Device pointers. */
+MAGIPLAN_API magiplan_status magiplan_debug_umma_tile(const void* a, const void* b, float* c,
+                                                      int32_t b_mn_major, void* cuda_stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MAGIPLAN_H */

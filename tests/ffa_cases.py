@@ -1,0 +1,60 @@
+"""Slice-list cases shared by the FFA parity tests (GPU vs the CPU oracle)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+FULL, CAUSAL, INV, BI = 0, 1, 2, 3
+
+
+def block_causal(seqlen, block):
+    qr = [[b, b + block] for b in range(0, seqlen, block)]
+    kr = [[0, b + block] for b in range(0, seqlen, block)]
+    return qr, kr, [FULL] * len(qr)
+
+
+def varlen(lengths, types):
+    qr, kr, off = [], [], 0
+    for n in lengths:
+        qr.append([off, off + n])
+        kr.append([off, off + n])
+        off += n
+    return qr, kr, list(types)
+
+
+# name -> (sq, sk, hq, hk, d, q_ranges, k_ranges, types)
+CASES = {
+    "cfg1_block_causal_d64": (1024, 1024, 1, 1, 64, *block_causal(1024, 256)),
+    "block_causal_gqa_d128": (1024, 1024, 4, 2, 128, *block_causal(1024, 256)),
+    "causal_unaligned": (300, 300, 2, 1, 128, [[0, 300]], [[0, 300]], [CAUSAL]),
+    "varlen_mixed": (512, 512, 2, 2, 128, *varlen([100, 37, 250, 125], [FULL, CAUSAL, FULL, CAUSAL])),
+    "inv_bi_d64": (384, 384, 2, 1, 64, [[0, 200], [200, 384]], [[0, 384], [50, 300]], [INV, BI]),
+    "overlap_multiplicity": (256, 256, 2, 2, 128, [[0, 256], [64, 192]], [[0, 256], [32, 160]],
+                             [FULL, CAUSAL]),
+    "empty_rows": (256, 256, 1, 1, 128, [[0, 100]], [[0, 256]], [FULL]),
+    "cross_lk_gt_lq": (200, 520, 2, 2, 128, [[0, 120], [120, 200]], [[0, 520], [100, 400]],
+                       [FULL, CAUSAL]),
+    "causal_lq_gt_lk": (400, 300, 1, 1, 64, [[0, 400]], [[0, 300]], [CAUSAL]),
+    "sliding_window": (640, 640, 2, 1, 128, [[0, 96], [96, 640]], [[0, 96], [1, 640]], [CAUSAL, BI]),
+}
+
+
+def make_inputs(sq, sk, hq, hk, d, seed=0, device="cuda"):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    q = torch.randn(sq, hq, d, generator=g).to(torch.bfloat16)
+    k = torch.randn(sk, hk, d, generator=g).to(torch.bfloat16)
+    v = torch.randn(sk, hk, d, generator=g).to(torch.bfloat16)
+    do = torch.randn(sq, hq, d, generator=g).to(torch.bfloat16)
+    return q.to(device), k.to(device), v.to(device), do.to(device)
+
+
+def err_stats(got: np.ndarray, ref: np.ndarray) -> tuple[float, float]:
+    """(max abs error, max abs error / max |ref|) over finite reference entries."""
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    fin = np.isfinite(ref)
+    if not fin.any():
+        return 0.0, 0.0
+    diff = np.abs(got[fin] - ref[fin])
+    scale = max(np.abs(ref[fin]).max(), 1e-12)
+    return float(diff.max()), float(diff.max() / scale)
