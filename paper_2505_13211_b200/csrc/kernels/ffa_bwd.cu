@@ -1,11 +1,648 @@
-// placeholder until the backward kernels land
+// FFA backward for sm_100a, deterministic (no unordered atomics).
+//
+// The five backward products of attention are split over two
+// kernels so every gradient element has exactly one producing CTA and one
+// fixed accumulation order:
+//
+//   dkdv kernel (k-major): one CTA per (128-key tile, key/value head). It walks
+//     every (q-head of the GQA group, slice item, q-tile) touching its keys:
+//       S^T  = K Q^T            (TMEM)       dP^T = V dO^T      (TMEM)
+//       P^T  = exp2(S^T*c - lse) (regs -> TMEM as packed bf16, aliasing S^T)
+//       dS^T = P^T (dP^T - delta)  (regs -> smem, bf16)
+//       dV  += P^T dO  (tcgen05.mma A-from-TMEM)   dK += dS^T Q  (SS)
+//     dK/dV stay in TMEM for the whole walk and are written once.
+//   dq kernel (q-major): one CTA per (128-query tile, q-head), the forward's
+//     work list: S = Q K^T, dP = dO V^T, dS = P (dP - delta), dQ += dS K.
+//
+// Warp roles in both: warps 0-3 elementwise (thread = TMEM lane = one row),
+// warp 4 TMA producer, warp 5 MMA issuer.
 #include <cuda_runtime.h>
+
+#include <cmath>
+
 #include "ffa_common.cuh"
+#include "sm100.cuh"
+#include "tma_host.h"
+
 namespace magi {
-cudaError_t launch_ffa_bwd(const FwdTile*, const FwdItem*, int, const BwdTile*, const BwdItem*, int,
-                           int, int, int, int, int, float, const void*, const void*, const void*,
-                           const float*, const float*, const void*, void*, void*, void*, int, int,
-                           cudaStream_t) {
-  return cudaErrorNotSupported;
+namespace {
+
+constexpr uint32_t kBox = 128 * 64 * 2;
+constexpr int kThreads = 192;
+constexpr int kMath = 128;
+constexpr float kLog2e = 1.4426950408889634f;
+
+struct BwdParams {
+  const FwdTile* q_tiles;
+  const FwdItem* q_items;
+  const BwdTile* k_tiles;
+  const BwdItem* k_items;
+  int32_t seqlen_q, seqlen_k;
+  int32_t hq, hk;
+  float scale, scale_log2;
+  const float* lse;
+  const float* delta;
+  void* dq;
+  void* dk;
+  void* dv;
+  int32_t grad_f32;
+  int32_t accumulate;
+};
+
+template <int D>
+__device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
+                                          int c, float scale, bool f32, bool accumulate) {
+  if (f32) {
+    float* dst = static_cast<float*>(base) + row_off + c * 32;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 a;
+      a.x = __uint_as_float(o[i + 0]) * scale;
+      a.y = __uint_as_float(o[i + 1]) * scale;
+      a.z = __uint_as_float(o[i + 2]) * scale;
+      a.w = __uint_as_float(o[i + 3]) * scale;
+      if (accumulate) {
+        const float4 b = *reinterpret_cast<const float4*>(dst + i);
+        a.x += b.x;
+        a.y += b.y;
+        a.z += b.z;
+        a.w += b.w;
+      }
+      *reinterpret_cast<float4*>(dst + i) = a;
+    }
+  } else {
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(base) + row_off + c * 32;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      uint4 v;
+      v.x = pack_bf16(__uint_as_float(o[i + 0]) * scale, __uint_as_float(o[i + 1]) * scale);
+      v.y = pack_bf16(__uint_as_float(o[i + 2]) * scale, __uint_as_float(o[i + 3]) * scale);
+      v.z = pack_bf16(__uint_as_float(o[i + 4]) * scale, __uint_as_float(o[i + 5]) * scale);
+      v.w = pack_bf16(__uint_as_float(o[i + 6]) * scale, __uint_as_float(o[i + 7]) * scale);
+      *reinterpret_cast<uint4*>(dst + i) = v;
+    }
+  }
 }
+
+// =========================================================================== dK / dV
+template <int D>
+struct DkvSmem {
+  static constexpr uint32_t kTile = (D / 64) * kBox;
+  static constexpr uint32_t kK = 0;
+  static constexpr uint32_t kV = kK + kTile;
+  static constexpr uint32_t kQ = kV + kTile;           // 2 stages
+  static constexpr uint32_t kDO = kQ + 2 * kTile;      // 2 stages
+  static constexpr uint32_t kDS = kDO + 2 * kTile;     // dS^T [keys, q] bf16, 2 boxes
+  static constexpr uint32_t kLse = kDS + 2 * kBox;      // [128] f32 (log2 domain)
+  static constexpr uint32_t kDelta = kLse + kBlockM * 4;
+  static constexpr uint32_t kBytes = kDelta + kBlockM * 4;
+};
+
+struct DkvBarriers {
+  uint64_t kv_full;
+  uint64_t qdo_full[2], qdo_empty[2];
+  uint64_t s_full, p_full, mma_done;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    ffa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                        const __grid_constant__ CUtensorMap tmap_k,
+                        const __grid_constant__ CUtensorMap tmap_v,
+                        const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
+  using L = DkvSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ DkvBarriers bars;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile_rank = blockIdx.x / p.hk;
+  const int head_k = blockIdx.x % p.hk;
+  const int group = p.hq / p.hk;
+  const BwdTile tile = p.k_tiles[tile_rank];
+  const int steps = tile.n_qtiles * group;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.qdo_full[s], 1);
+      mbar_init(&bars.qdo_empty[s], 1);
+    }
+    mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.p_full, kMath);
+    mbar_init(&bars.mma_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t t_st = tmem;          // S^T, then packed P^T in its first 64 columns
+  const uint32_t t_dpt = tmem + 128;   // dP^T
+  const uint32_t t_dv = tmem + 256;    // dV  [keys, D]
+  const uint32_t t_dk = tmem + 256 + D;  // dK [keys, D]
+
+  uint8_t* sK = smem + L::kK;
+  uint8_t* sV = smem + L::kV;
+  uint8_t* sQ = smem + L::kQ;
+  uint8_t* sDO = smem + L::kDO;
+  uint8_t* sDS = smem + L::kDS;
+  float* s_lse = reinterpret_cast<float*>(smem + L::kLse);
+  float* s_delta = reinterpret_cast<float*>(smem + L::kDelta);
+
+  if (warp == 4) {
+    if (lane == 0 && steps > 0) {
+      tma_prefetch_desc(&tmap_q);
+      tma_prefetch_desc(&tmap_do);
+      mbar_arrive_expect_tx(&bars.kv_full, 2 * L::kTile);
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_3d(sK + c * kBox, &tmap_k, &bars.kv_full, c * 64, head_k, tile.k0);
+        tma_load_3d(sV + c * kBox, &tmap_v, &bars.kv_full, c * 64, head_k, tile.k0);
+      }
+      PipeState st;
+      for (int g = 0; g < group; ++g) {
+        const int h = head_k * group + g;
+        for (int it = tile.item_begin; it < tile.item_end; ++it) {
+          const BwdItem item = p.k_items[it];
+          for (int i = 0; i < item.n_qtiles; ++i) {
+            const int q0 = item.q_begin + i * kBlockM;
+            mbar_wait(&bars.qdo_empty[st.index], st.phase ^ 1);
+            mbar_arrive_expect_tx(&bars.qdo_full[st.index], 2 * L::kTile);
+            for (int c = 0; c < D / 64; ++c) {
+              tma_load_3d(sQ + st.index * L::kTile + c * kBox, &tmap_q, &bars.qdo_full[st.index],
+                          c * 64, h, q0);
+              tma_load_3d(sDO + st.index * L::kTile + c * kBox, &tmap_do,
+                          &bars.qdo_full[st.index], c * 64, h, q0);
+            }
+            st.advance<2>();
+          }
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && steps > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_g = make_idesc_bf16(128, D, false, true);
+      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sDS);
+      mbar_wait(&bars.kv_full, 0);
+      PipeState st;
+      for (int t = 0; t < steps; ++t) {
+        mbar_wait(&bars.qdo_full[st.index], st.phase);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + st.index * L::kTile);
+        const uint32_t do_addr = smem_u32(sDO + st.index * L::kTile);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+          umma_bf16_ss(t_st, make_smem_desc(k_addr + off, 16, 1024),
+                       make_smem_desc(q_addr + off, 16, 1024), idesc_s, k > 0);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+          umma_bf16_ss(t_dpt, make_smem_desc(v_addr + off, 16, 1024),
+                       make_smem_desc(do_addr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(&bars.s_full);
+        mbar_wait(&bars.p_full, t & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < kBlockM / 16; ++k) {
+          // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] (MN-major)
+          umma_bf16_ts(t_dv, t_st + k * 8, make_smem_desc(do_addr + k * 16 * 128, kBox, 1024),
+                       idesc_g, (t > 0 || k > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < kBlockM / 16; ++k) {
+          // dK += dS^T Q : A = dS^T [keys, q] (K-major smem), B = Q [q, D] (MN-major)
+          umma_bf16_ss(t_dk, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
+                       make_smem_desc(q_addr + k * 16 * 128, kBox, 1024), idesc_g,
+                       (t > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&bars.mma_done);
+        umma_commit(&bars.qdo_empty[st.index]);
+        st.advance<2>();
+      }
+    }
+  } else {
+    const int row = warp * 32 + lane;
+    const int key = tile.k0 + row;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    int t = 0;
+    for (int g = 0; g < group; ++g) {
+      const int h = head_k * group + g;
+      const float* lse_h = p.lse + static_cast<size_t>(h) * p.seqlen_q;
+      const float* delta_h = p.delta + static_cast<size_t>(h) * p.seqlen_q;
+      for (int it = tile.item_begin; it < tile.item_end; ++it) {
+        const BwdItem item = p.k_items[it];
+        // rows of this slice that may attend `key`: [qlo, qhi)
+        int qlo = item.qs, qhi = item.qe;
+        if (key < item.ks || key >= item.ke) {
+          qhi = qlo;
+        } else {
+          if (item.type == kCausal || item.type == kBiCausal) qlo = max(qlo, key - (item.ke - item.qe));
+          if (item.type == kInvCausal || item.type == kBiCausal) qhi = min(qhi, key - item.ks + item.qs + 1);
+        }
+        for (int i = 0; i < item.n_qtiles; ++i, ++t) {
+          const int q0 = item.q_begin + i * kBlockM;
+          // every math thread is done reading the previous step's lse/delta
+          named_bar_sync(1, kMath);
+          {
+            const int qq = q0 + row;
+            float l = INFINITY, dlt = 0.f;
+            if (qq < p.seqlen_q) {
+              const float raw = lse_h[qq];
+              l = raw == -INFINITY ? INFINITY : raw * kLog2e;
+              dlt = delta_h[qq];
+            }
+            s_lse[row] = l;
+            s_delta[row] = dlt;
+          }
+          named_bar_sync(1, kMath);
+          mbar_wait(&bars.s_full, t & 1);
+          // keeps this thread at most one mma_done phase behind, so the final
+          // parity wait below cannot alias an older phase
+          if (t > 0) mbar_wait(&bars.mma_done, (t - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < kBlockM / 32; ++c) {
+            uint32_t s[32], dp[32];
+            tmem_ld32(t_st + lane_off + c * 32, s);
+            tmem_ld32(t_dpt + lane_off + c * 32, dp);
+            tmem_ld_wait();
+            uint32_t pk[16], dk[16];
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              float pv[2], dv[2];
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int col = c * 32 + j + u;
+                const int qq = q0 + col;
+                const bool ok = qq >= qlo && qq < qhi;
+                const float e = fast_exp2(__uint_as_float(s[j + u]) * p.scale_log2 - s_lse[col]);
+                pv[u] = ok ? e : 0.f;
+                dv[u] = pv[u] * (__uint_as_float(dp[j + u]) - s_delta[col]);
+              }
+              pk[j / 2] = pack_bf16(pv[0], pv[1]);
+              dk[j / 2] = pack_bf16(dv[0], dv[1]);
+            }
+            // P^T chunk -> TMEM columns [c*16, c*16+16) (already-consumed S^T columns)
+            uint32_t pk32[32];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk32[j] = pk[j];
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+                "%12,%13,%14,%15,%16};" ::"r"(t_st + lane_off + c * 16),
+                "r"(pk32[0]), "r"(pk32[1]), "r"(pk32[2]), "r"(pk32[3]), "r"(pk32[4]), "r"(pk32[5]),
+                "r"(pk32[6]), "r"(pk32[7]), "r"(pk32[8]), "r"(pk32[9]), "r"(pk32[10]),
+                "r"(pk32[11]), "r"(pk32[12]), "r"(pk32[13]), "r"(pk32[14]), "r"(pk32[15])
+                : "memory");
+            // dS^T chunk -> smem row `row`, q columns [c*32, c*32+32)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int chunk16 = c * 4 + u;  // 16-byte chunk index over 128 q columns
+              uint4 v = make_uint4(dk[u * 4 + 0], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3]);
+              *reinterpret_cast<uint4*>(sDS + (chunk16 / 8) * kBox + sw128_offset(row, chunk16 % 8)) = v;
+            }
+          }
+          tmem_st_wait();
+          fence_proxy_async_smem();
+          tc_fence_before();
+          mbar_arrive(&bars.p_full);
+        }
+      }
+    }
+    // epilogue: dV, dK rows
+    if (steps > 0) {
+      mbar_wait(&bars.mma_done, (steps - 1) & 1);
+      tc_fence_after();
+    }
+    const bool valid = key < p.seqlen_k;
+    const size_t row_off = (static_cast<size_t>(key) * p.hk + head_k) * D;
+    const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      if (steps > 0) {
+        tmem_ld32(t_dv + lane_off + c * 32, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0u;
+      }
+      if (valid && !(acc && steps == 0)) store_row<D>(p.dv, row_off, o, c, 1.f, f32, acc);
+    }
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      if (steps > 0) {
+        tmem_ld32(t_dk + lane_off + c * 32, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0u;
+      }
+      if (valid && !(acc && steps == 0)) store_row<D>(p.dk, row_off, o, c, p.scale, f32, acc);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+// =========================================================================== dQ
+template <int D>
+struct DqSmem {
+  static constexpr uint32_t kTile = (D / 64) * kBox;
+  static constexpr uint32_t kQ = 0;
+  static constexpr uint32_t kDO = kQ + kTile;
+  static constexpr uint32_t kK = kDO + kTile;       // 2 stages
+  static constexpr uint32_t kV = kK + 2 * kTile;    // 2 stages
+  static constexpr uint32_t kDS = kV + 2 * kTile;   // dS [q, keys] bf16, 2 boxes
+  static constexpr uint32_t kBytes = kDS + 2 * kBox;
+};
+
+struct DqBarriers {
+  uint64_t qdo_full;
+  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+  uint64_t s_full, s_free, ds_full, dq_done;
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    ffa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmap_q,
+                      const __grid_constant__ CUtensorMap tmap_k,
+                      const __grid_constant__ CUtensorMap tmap_v,
+                      const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
+  using L = DqSmem<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  __shared__ DqBarriers bars;
+  __shared__ uint32_t tmem_slot;
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tile_rank = blockIdx.x / p.hq;
+  const int head = blockIdx.x % p.hq;
+  const int head_k = head / (p.hq / p.hk);
+  const FwdTile tile = p.q_tiles[tile_rank];
+  const int steps = tile.n_ktiles;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bars.qdo_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars.k_full[s], 1);
+      mbar_init(&bars.k_empty[s], 1);
+      mbar_init(&bars.v_full[s], 1);
+      mbar_init(&bars.v_empty[s], 1);
+    }
+    mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.s_free, kMath);
+    mbar_init(&bars.ds_full, kMath);
+    mbar_init(&bars.dq_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(&tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+
+  uint8_t* sQ = smem + L::kQ;
+  uint8_t* sDO = smem + L::kDO;
+  uint8_t* sK = smem + L::kK;
+  uint8_t* sV = smem + L::kV;
+  uint8_t* sDS = smem + L::kDS;
+
+  if (warp == 4) {
+    if (lane == 0 && steps > 0) {
+      tma_prefetch_desc(&tmap_k);
+      tma_prefetch_desc(&tmap_v);
+      mbar_arrive_expect_tx(&bars.qdo_full, 2 * L::kTile);
+      for (int c = 0; c < D / 64; ++c) {
+        tma_load_3d(sQ + c * kBox, &tmap_q, &bars.qdo_full, c * 64, head, tile.q0);
+        tma_load_3d(sDO + c * kBox, &tmap_do, &bars.qdo_full, c * 64, head, tile.q0);
+      }
+      PipeState st;
+      for (int it = tile.item_begin; it < tile.item_end; ++it) {
+        const FwdItem item = p.q_items[it];
+        for (int j = 0; j < item.n_ktiles; ++j) {
+          const int k0 = item.k_begin + j * kBlockN;
+          mbar_wait(&bars.k_empty[st.index], st.phase ^ 1);
+          mbar_arrive_expect_tx(&bars.k_full[st.index], L::kTile);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(sK + st.index * L::kTile + c * kBox, &tmap_k, &bars.k_full[st.index],
+                        c * 64, head_k, k0);
+          mbar_wait(&bars.v_empty[st.index], st.phase ^ 1);
+          mbar_arrive_expect_tx(&bars.v_full[st.index], L::kTile);
+          for (int c = 0; c < D / 64; ++c)
+            tma_load_3d(sV + st.index * L::kTile + c * kBox, &tmap_v, &bars.v_full[st.index],
+                        c * 64, head_k, k0);
+          st.advance<2>();
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0 && steps > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idesc_q = make_idesc_bf16(128, D, false, true);
+      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
+      mbar_wait(&bars.qdo_full, 0);
+      PipeState kst, vst;
+      auto issue_s = [&](int t) {
+        if (t > 0) mbar_wait(&bars.s_free, (t - 1) & 1);
+        mbar_wait(&bars.k_full[kst.index], kst.phase);
+        mbar_wait(&bars.v_full[vst.index], vst.phase);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + kst.index * L::kTile);
+        const uint32_t v_addr = smem_u32(sV + vst.index * L::kTile);
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+          umma_bf16_ss(t_s, make_smem_desc(q_addr + off, 16, 1024),
+                       make_smem_desc(k_addr + off, 16, 1024), idesc_s, k > 0);
+        }
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+          umma_bf16_ss(t_dp, make_smem_desc(do_addr + off, 16, 1024),
+                       make_smem_desc(v_addr + off, 16, 1024), idesc_s, k > 0);
+        }
+        umma_commit(&bars.s_full);
+        umma_commit(&bars.v_empty[vst.index]);
+        vst.advance<2>();
+      };
+      issue_s(0);
+      PipeState kuse;  // stage of the K tile dQ_t consumes
+      for (int t = 0; t < steps; ++t) {
+        const PipeState kcur = kuse;
+        kst.advance<2>();
+        if (t + 1 < steps) issue_s(t + 1);
+        mbar_wait(&bars.ds_full, t & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(sK + kcur.index * L::kTile);
+#pragma unroll
+        for (int k = 0; k < kBlockN / 16; ++k) {
+          // dQ += dS K : A = dS [q, keys] K-major, B = K [keys, D] MN-major
+          umma_bf16_ss(t_dq, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
+                       make_smem_desc(k_addr + k * 16 * 128, kBox, 1024), idesc_q,
+                       (t > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&bars.dq_done);
+        umma_commit(&bars.k_empty[kcur.index]);
+        kuse.advance<2>();
+      }
+    }
+  } else {
+    const int row = warp * 32 + lane;
+    const int q = tile.q0 + row;
+    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const bool valid = q < p.seqlen_q;
+    float lse_l2 = INFINITY, dlt = 0.f;
+    if (valid) {
+      const float raw = p.lse[static_cast<size_t>(head) * p.seqlen_q + q];
+      lse_l2 = raw == -INFINITY ? INFINITY : raw * kLog2e;
+      dlt = p.delta[static_cast<size_t>(head) * p.seqlen_q + q];
+    }
+    int t = 0;
+    for (int it = tile.item_begin; it < tile.item_end; ++it) {
+      const FwdItem item = p.q_items[it];
+      int32_t lo, hi;
+      row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q, lo, hi);
+      for (int j = 0; j < item.n_ktiles; ++j, ++t) {
+        const int k0 = item.k_begin + j * kBlockN;
+        mbar_wait(&bars.s_full, t & 1);
+        tc_fence_after();
+        uint32_t ds[64];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t s[32], dp[32];
+          tmem_ld32(t_s + lane_off + c * 32, s);
+          tmem_ld32(t_dp + lane_off + c * 32, dp);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float v2[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int col = k0 + c * 32 + i + u;
+              const bool ok = col >= lo && col < hi;
+              const float e = fast_exp2(__uint_as_float(s[i + u]) * p.scale_log2 - lse_l2);
+              v2[u] = ok ? e * (__uint_as_float(dp[i + u]) - dlt) : 0.f;
+            }
+            ds[c * 16 + i / 2] = pack_bf16(v2[0], v2[1]);
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&bars.s_free);
+        if (t > 0) mbar_wait(&bars.dq_done, (t - 1) & 1);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) {
+          *reinterpret_cast<uint4*>(sDS + (c / 8) * kBox + sw128_offset(row, c % 8)) =
+              make_uint4(ds[c * 4 + 0], ds[c * 4 + 1], ds[c * 4 + 2], ds[c * 4 + 3]);
+        }
+        fence_proxy_async_smem();
+        tc_fence_before();
+        mbar_arrive(&bars.ds_full);
+      }
+    }
+    if (steps > 0) {
+      mbar_wait(&bars.dq_done, (steps - 1) & 1);
+      tc_fence_after();
+    }
+    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D;
+    const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
+#pragma unroll 1
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      if (steps > 0) {
+        tmem_ld32(t_dq + lane_off + c * 32, o);
+        tmem_ld_wait();
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = 0u;
+      }
+      if (valid && !(acc && steps == 0)) store_row<D>(p.dq, row_off, o, c, p.scale, f32, acc);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int D>
+cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_tiles,
+                            const void* q, const void* k, const void* v, const void* dout,
+                            cudaStream_t stream) {
+  const CUtensorMap tq = make_tmap_thd(q, prm.seqlen_q, prm.hq, D, 128);
+  const CUtensorMap tdo = make_tmap_thd(dout, prm.seqlen_q, prm.hq, D, 128);
+  const CUtensorMap tk = make_tmap_thd(k, prm.seqlen_k, prm.hk, D, 128);
+  const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
+  cudaError_t err;
+  if (num_k_tiles > 0) {
+    const int smem = DkvSmem<D>::kBytes + 1024;
+    err = cudaFuncSetAttribute(ffa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem);
+    if (err != cudaSuccess) return err;
+    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kThreads, smem, stream>>>(tq, tk, tv, tdo,
+                                                                                   prm);
+    err = cudaGetLastError();
+    if (err != cudaSuccess) return err;
+  }
+  if (num_q_tiles > 0) {
+    const int smem = DqSmem<D>::kBytes + 1024;
+    err = cudaFuncSetAttribute(ffa_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               smem);
+    if (err != cudaSuccess) return err;
+    ffa_bwd_dq_kernel<D><<<dim3(num_q_tiles * prm.hq), kThreads, smem, stream>>>(tq, tk, tv, tdo,
+                                                                                 prm);
+    err = cudaGetLastError();
+  }
+  return err == cudaSuccess ? cudaGetLastError() : err;
+}
+
+}  // namespace
+
+cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int num_q_tiles,
+                           const BwdTile* k_tiles, const BwdItem* k_items, int num_k_tiles,
+                           int seqlen_q, int seqlen_k, int hq, int hk, int head_dim,
+                           float softmax_scale, const void* q, const void* k, const void* v,
+                           const float* lse, const float* delta, const void* grad_out,
+                           void* grad_q, void* grad_k, void* grad_v, int grad_f32,
+                           int accumulate, cudaStream_t stream) {
+  BwdParams prm;
+  prm.q_tiles = q_tiles;
+  prm.q_items = q_items;
+  prm.k_tiles = k_tiles;
+  prm.k_items = k_items;
+  prm.seqlen_q = seqlen_q;
+  prm.seqlen_k = seqlen_k;
+  prm.hq = hq;
+  prm.hk = hk;
+  prm.scale = softmax_scale;
+  prm.scale_log2 = softmax_scale * kLog2e;
+  prm.lse = lse;
+  prm.delta = delta;
+  prm.dq = grad_q;
+  prm.dk = grad_k;
+  prm.dv = grad_v;
+  prm.grad_f32 = grad_f32;
+  prm.accumulate = accumulate;
+  if (head_dim == 128) return launch_bwd_impl<128>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, stream);
+  if (head_dim == 64) return launch_bwd_impl<64>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, stream);
+  return cudaErrorInvalidValue;
+}
+
 }  // namespace magi
