@@ -156,6 +156,24 @@ MAGIPLAN_API magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, con
                                               float softmax_scale, int32_t grad_dtype,
                                               int32_t accumulate, void* cuda_stream);
 
+/* The two halves of magiplan_ffa_bwd, for per-kernel timing and for running
+ * them on separate streams: the k-major dK/dV pass and the q-major dQ pass. */
+MAGIPLAN_API magiplan_status magiplan_ffa_bwd_dkdv(const magiplan_ffa_plan* plan, const void* q,
+                                                   const void* k, const void* v,
+                                                   const float* lse, const float* delta,
+                                                   const void* grad_out, void* grad_k,
+                                                   void* grad_v, int64_t num_heads_q,
+                                                   int64_t num_heads_k, float softmax_scale,
+                                                   int32_t grad_dtype, int32_t accumulate,
+                                                   void* cuda_stream);
+MAGIPLAN_API magiplan_status magiplan_ffa_bwd_dq(const magiplan_ffa_plan* plan, const void* q,
+                                                 const void* k, const void* v, const float* lse,
+                                                 const float* delta, const void* grad_out,
+                                                 void* grad_q, int64_t num_heads_q,
+                                                 int64_t num_heads_k, float softmax_scale,
+                                                 int32_t grad_dtype, int32_t accumulate,
+                                                 void* cuda_stream);
+
 /* ---- context-parallel data movement kernels (new) ---------------------- */
 /* Gather token ranges of a [tokens, width] row-major buffer into a packed
  * buffer (Range Gather). ranges: device int64 [n][2];

@@ -25,7 +25,7 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
                            float softmax_scale, const void* q, const void* k, const void* v,
                            const float* lse, const float* delta, const void* grad_out,
                            void* grad_q, void* grad_k, void* grad_v, int grad_f32,
-                           int accumulate, cudaStream_t stream);
+                           int accumulate, int parts, cudaStream_t stream);
 cudaError_t launch_range_gather(const void* src, void* dst, const int64_t* ranges,
                                 const int64_t* offsets, int64_t num_ranges, int64_t total_rows,
                                 int64_t row_bytes, cudaStream_t stream);
@@ -169,12 +169,13 @@ magiplan_status magiplan_ffa_bwd_preprocess(const void* out, const void* grad_ou
   });
 }
 
-magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, const void* q, const void* k,
-                                 const void* v, const float* lse, const float* delta,
-                                 const void* grad_out, void* grad_q, void* grad_k, void* grad_v,
-                                 int64_t num_heads_q, int64_t num_heads_k, float softmax_scale,
-                                 int32_t grad_dtype, int32_t accumulate, void* cuda_stream) {
-  MAGI_REQUIRE(plan && q && k && v && lse && delta && grad_out && grad_q && grad_k && grad_v);
+namespace {
+magiplan_status ffa_bwd_parts(const magiplan_ffa_plan* plan, const void* q, const void* k,
+                              const void* v, const float* lse, const float* delta,
+                              const void* grad_out, void* grad_q, void* grad_k, void* grad_v,
+                              int64_t num_heads_q, int64_t num_heads_k, float softmax_scale,
+                              int32_t grad_dtype, int32_t accumulate, int parts,
+                              void* cuda_stream) {
   return guarded([&] {
     check_heads(num_heads_q, num_heads_k);
     check_dtype(grad_dtype, accumulate);
@@ -185,10 +186,42 @@ magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, const void* q, c
                              static_cast<int>(P.seqlen_q), static_cast<int>(P.seqlen_k),
                              static_cast<int>(num_heads_q), static_cast<int>(num_heads_k),
                              P.head_dim, softmax_scale, q, k, v, lse, delta, grad_out, grad_q,
-                             grad_k, grad_v, grad_dtype == MAGIPLAN_F32, accumulate != 0,
+                             grad_k, grad_v, grad_dtype == MAGIPLAN_F32, accumulate != 0, parts,
                              as_stream(cuda_stream)),
         "ffa_bwd launch");
   });
+}
+}  // namespace
+
+magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, const void* q, const void* k,
+                                 const void* v, const float* lse, const float* delta,
+                                 const void* grad_out, void* grad_q, void* grad_k, void* grad_v,
+                                 int64_t num_heads_q, int64_t num_heads_k, float softmax_scale,
+                                 int32_t grad_dtype, int32_t accumulate, void* cuda_stream) {
+  MAGI_REQUIRE(plan && q && k && v && lse && delta && grad_out && grad_q && grad_k && grad_v);
+  return ffa_bwd_parts(plan, q, k, v, lse, delta, grad_out, grad_q, grad_k, grad_v, num_heads_q,
+                       num_heads_k, softmax_scale, grad_dtype, accumulate, 3, cuda_stream);
+}
+
+magiplan_status magiplan_ffa_bwd_dkdv(const magiplan_ffa_plan* plan, const void* q,
+                                      const void* k, const void* v, const float* lse,
+                                      const float* delta, const void* grad_out, void* grad_k,
+                                      void* grad_v, int64_t num_heads_q, int64_t num_heads_k,
+                                      float softmax_scale, int32_t grad_dtype,
+                                      int32_t accumulate, void* cuda_stream) {
+  MAGI_REQUIRE(plan && q && k && v && lse && delta && grad_out && grad_k && grad_v);
+  return ffa_bwd_parts(plan, q, k, v, lse, delta, grad_out, grad_k, grad_k, grad_v, num_heads_q,
+                       num_heads_k, softmax_scale, grad_dtype, accumulate, 1, cuda_stream);
+}
+
+magiplan_status magiplan_ffa_bwd_dq(const magiplan_ffa_plan* plan, const void* q, const void* k,
+                                    const void* v, const float* lse, const float* delta,
+                                    const void* grad_out, void* grad_q, int64_t num_heads_q,
+                                    int64_t num_heads_k, float softmax_scale, int32_t grad_dtype,
+                                    int32_t accumulate, void* cuda_stream) {
+  MAGI_REQUIRE(plan && q && k && v && lse && delta && grad_out && grad_q);
+  return ffa_bwd_parts(plan, q, k, v, lse, delta, grad_out, grad_q, grad_q, grad_q, num_heads_q,
+                       num_heads_k, softmax_scale, grad_dtype, accumulate, 2, cuda_stream);
 }
 
 magiplan_status magiplan_range_gather(const void* src, void* dst, const int64_t* ranges,

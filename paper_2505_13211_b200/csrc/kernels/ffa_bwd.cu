@@ -585,13 +585,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int D>
 cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_tiles,
                             const void* q, const void* k, const void* v, const void* dout,
-                            cudaStream_t stream) {
+                            int parts, cudaStream_t stream) {
   const CUtensorMap tq = make_tmap_thd(q, prm.seqlen_q, prm.hq, D, 128);
   const CUtensorMap tdo = make_tmap_thd(dout, prm.seqlen_q, prm.hq, D, 128);
   const CUtensorMap tk = make_tmap_thd(k, prm.seqlen_k, prm.hk, D, 128);
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
-  cudaError_t err;
-  if (num_k_tiles > 0) {
+  cudaError_t err = cudaSuccess;
+  if ((parts & 1) && num_k_tiles > 0) {
     const int smem = DkvSmem<D>::kBytes + 1024;
     err = cudaFuncSetAttribute(ffa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
@@ -601,7 +601,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
-  if (num_q_tiles > 0) {
+  if ((parts & 2) && num_q_tiles > 0) {
     const int smem = DqSmem<D>::kBytes + 1024;
     err = cudaFuncSetAttribute(ffa_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
@@ -621,7 +621,7 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
                            float softmax_scale, const void* q, const void* k, const void* v,
                            const float* lse, const float* delta, const void* grad_out,
                            void* grad_q, void* grad_k, void* grad_v, int grad_f32,
-                           int accumulate, cudaStream_t stream) {
+                           int accumulate, int parts, cudaStream_t stream) {
   BwdParams prm;
   prm.q_tiles = q_tiles;
   prm.q_items = q_items;
@@ -640,8 +640,8 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.dv = grad_v;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
-  if (head_dim == 128) return launch_bwd_impl<128>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, stream);
-  if (head_dim == 64) return launch_bwd_impl<64>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, stream);
+  if (head_dim == 128) return launch_bwd_impl<128>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
+  if (head_dim == 64) return launch_bwd_impl<64>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
   return cudaErrorInvalidValue;
 }
 
