@@ -196,6 +196,12 @@ MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst,
                                                     void* cuda_stream);
 
 /* ---- diagnostics ------------------------------------------------------- */
+/* JSON-RPC access to individual planner functions for parity tests:
+ * {"op": "slice_area" | "slice_area_in_cols" | "clip_slice" | "mask" |
+ *  "restrict_rows" | "shard" | "greedy" | "zigzag" | "brute_force" |
+ *  "demands" | "partition_packages" | "assign_packages" | "estimate" |
+ *  "fit_affine" | "lognormal" | "flops", ...}. */
+MAGIPLAN_API magiplan_status magiplan_debug_eval(const char* request_json, char** out_json);
 /* One 128x128x128 bf16 tile product through the TMA/UMMA building blocks
  * (C = A B^T for b_mn_major == 0, C = A B otherwise). Device pointers. */
 MAGIPLAN_API magiplan_status magiplan_debug_umma_tile(const void* a, const void* b, float* c,

@@ -1,0 +1,132 @@
+// JSON-RPC access to individual planner functions (magiplan_debug_eval), so
+// the parity tests can replay the reference's golden vectors function by
+// function. Request: {"op": name, ...args}; response: JSON value.
+#include <nlohmann/json.hpp>
+
+#include "errors.hpp"
+#include "scenario.hpp"
+
+namespace magiplan {
+
+using json = nlohmann::ordered_json;
+
+namespace {
+
+AttnSlice slice_of(const json& s) {
+  return {{s[0].get<Token>(), s[1].get<Token>()}, {s[2].get<Token>(), s[3].get<Token>()},
+          static_cast<SliceType>(s[4].get<int>())};
+}
+
+json slice_json(const AttnSlice& s) {
+  return json::array({s.q.start, s.q.end, s.k.start, s.k.end, static_cast<int>(s.type)});
+}
+
+AttnMask mask_of(const json& j) { return parse_mask_spec(j.dump()); }
+
+std::vector<DispatchChunk> chunks_of(const json& areas) {
+  std::vector<DispatchChunk> c;
+  int64_t i = 0;
+  for (const auto& a : areas) {
+    c.push_back({i, {i, i + 1}, a.get<Pairs>()});
+    ++i;
+  }
+  return c;
+}
+
+json plan_json(const DispatchPlan& p) {
+  return {{"assignment", p.assignment}, {"workloads", p.bucket_workloads}};
+}
+
+DispatchPlan plan_of(const json& r) {
+  DispatchPlan p;
+  p.cp_size = r["cp"].get<Rank>();
+  p.chunk_size = r["chunk"].get<Token>();
+  p.assignment = r["assignment"].get<std::vector<Rank>>();
+  p.bucket_workloads.assign(static_cast<std::size_t>(p.cp_size), 0);
+  return p;
+}
+
+}  // namespace
+
+std::string debug_eval(const std::string& request) {
+  json r;
+  try {
+    r = json::parse(request);
+  } catch (const nlohmann::json::exception& e) {
+    throw UsageError(std::string("debug request: ") + e.what());
+  }
+  const std::string op = r.value("op", "");
+  json out;
+  if (op == "slice_area") {
+    out = slice_area(slice_of(r["slice"]));
+  } else if (op == "slice_area_in_cols") {
+    out = slice_area_in_cols(slice_of(r["slice"]), r["cols"][0].get<Token>(), r["cols"][1].get<Token>());
+  } else if (op == "clip_slice") {
+    out = json::array();
+    for (const auto& p : clip_slice(slice_of(r["slice"]), {r["rows"][0].get<Token>(), r["rows"][1].get<Token>()},
+                                    {r["cols"][0].get<Token>(), r["cols"][1].get<Token>()}))
+      out.push_back(slice_json(p));
+  } else if (op == "mask") {
+    const AttnMask m = mask_of(r["mask"]);
+    out["json"] = json::parse(mask_to_json(m));
+    out["area_union"] = mask_area(m, Counting::Union);
+    out["area_multiplicity"] = mask_area(m, Counting::Multiplicity);
+    if (r.value("rows", false)) out["row_counts"] = union_row_counts(m);
+  } else if (op == "restrict_rows") {
+    std::vector<TokenRange> rows;
+    for (const auto& x : r["rows"]) rows.push_back({x[0].get<Token>(), x[1].get<Token>()});
+    out = json::parse(mask_to_json(restrict_rows(mask_of(r["mask"]), rows)));
+  } else if (op == "shard") {
+    out = json::array();
+    for (const auto& c : shard_into_chunks(mask_of(r["mask"]), r["chunk"].get<Token>())) out.push_back(c.area);
+  } else if (op == "greedy" || op == "zigzag" || op == "brute_force") {
+    const auto ch = chunks_of(r["areas"]);
+    const Rank cp = r["cp"].get<Rank>();
+    out = plan_json(op == "greedy" ? greedy_dispatch(ch, cp)
+                                   : op == "zigzag" ? zigzag_dispatch(ch, cp) : brute_force_dispatch(ch, cp));
+  } else if (op == "demands") {
+    const DispatchPlan p = plan_of(r);
+    const auto d = compute_kv_demands(mask_of(r["mask"]), p);
+    json jd = json::array();
+    for (const auto& x : d) jd.push_back({x.host_rank, x.consumers});
+    const auto [cast, reduce] = build_transfer_tables(d, p.chunk_size, p.cp_size);
+    out["demands"] = jd;
+    out["cast"] = json::parse(transfer_table_to_json(cast, 1));
+    out["reduce"] = json::parse(transfer_table_to_json(reduce, 1));
+    const auto rr = redundancy_report(d, p);
+    out["redundancy"] = {rr.sent_ring, rr.needed, rr.sent_group};
+  } else if (op == "partition_packages") {
+    out = partition_packages(r["traffic"].get<std::vector<int64_t>>(), r["min"].get<int64_t>(),
+                             r["max"].get<int64_t>());
+  } else if (op == "assign_packages") {
+    std::optional<uint64_t> seed;
+    if (r.contains("seed")) seed = r["seed"].get<uint64_t>();
+    out = assign_packages_to_stages(r["sizes"].get<std::vector<int64_t>>(), r["stages"].get<int>(), seed);
+  } else if (op == "estimate") {
+    StageCosts c;
+    c.host_compute = r["host"].get<Cost>();
+    c.compute = r["compute"].get<std::vector<Cost>>();
+    c.cast = r["cast"].get<std::vector<Cost>>();
+    c.reduce = r["reduce"].get<std::vector<Cost>>();
+    out = {estimate_fwd_cost(c), estimate_bwd_cost(c)};
+  } else if (op == "fit_affine") {
+    const auto f = fit_affine(r["samples"].get<std::vector<std::pair<int64_t, int64_t>>>());
+    out = {f.latency, f.per_unit};
+  } else if (op == "lognormal") {
+    out = lognormal_lengths(r["count"].get<std::size_t>(), r["median"].get<double>(),
+                            r["sigma"].get<double>(), r["max_length"].get<Token>(),
+                            r["seed"].get<uint64_t>());
+  } else if (op == "flops") {
+    WorkloadSpec w;
+    w.num_heads_q = r["num_heads_q"].get<int64_t>();
+    w.head_dim = r["head_dim"].get<int64_t>();
+    w.batch_size = r.value("batch_size", int64_t{1});
+    const AttnMask m = mask_of(r["mask"]);
+    out = {flops(m, w, Pass::Fwd), flops(m, w, Pass::Bwd)};
+  } else {
+    throw UsageError("unknown debug op '" + op + "'");
+  }
+  return out.dump();
+}
+
+}  // namespace magiplan

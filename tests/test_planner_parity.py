@@ -1,0 +1,119 @@
+"""Planner parity (CPU): every golden record produced by the compiled
+reference planner (oracle/ref_golden.cpp -> tests/golden/ref_planner.json)
+is replayed through libmagiplan.so and must agree exactly: integer areas,
+slice lists, dispatch assignments, demand sets, transfer tables, package /
+stage plans, and byte-identical plan / simulate JSON."""
+import json
+from pathlib import Path
+
+import pytest
+
+GOLD = json.loads((Path(__file__).parent / "golden" / "ref_planner.json").read_text())
+
+
+@pytest.fixture(scope="module")
+def P(built_lib):
+    from paper_2505_13211_b200 import planner
+
+    return planner
+
+
+def test_slice_area(P):
+    for s, area in GOLD["slice_area"]:
+        assert P.debug_eval("slice_area", slice=s) == area, s
+
+
+def test_slice_area_in_cols(P):
+    for s, cols, area in GOLD["slice_area_in_cols"]:
+        assert P.debug_eval("slice_area_in_cols", slice=s, cols=cols) == area, (s, cols)
+
+
+def test_named_masks(P):
+    for e in GOLD["named_masks"]:
+        got = P.debug_eval("mask", mask=e["spec"], rows="row_counts" in e)
+        assert got["json"] == e["json"]
+        assert got["area_union"] == e["area_union"]
+        assert got["area_multiplicity"] == e["area_multiplicity"]
+        if "row_counts" in e:
+            assert got["row_counts"] == e["row_counts"]
+        if "ascii" in e:
+            assert P.Mask(e["spec"]).render() == e["ascii"]
+
+
+def test_random_masks_union_and_restrict(P):
+    for e in GOLD["random_masks"]:
+        got = P.debug_eval("mask", mask=e["mask"], rows=True)
+        assert got["area_union"] == e["area_union"]
+        assert got["area_multiplicity"] == e["area_multiplicity"]
+        assert got["row_counts"] == e["row_counts"]
+        assert P.debug_eval("restrict_rows", mask=e["mask"], rows=e["rows"]) == e["restricted"]
+
+
+def test_dispatch_bit_exact(P):
+    for e in GOLD["dispatch"]:
+        for op in ("greedy", "zigzag", "brute_force"):
+            if op in e:
+                assert P.debug_eval(op, areas=e["areas"], cp=e["cp"]) == e[op], (op, e["areas"], e["cp"])
+
+
+def test_demands_and_tables(P):
+    for e in GOLD["demands"]:
+        assert P.debug_eval("shard", mask=e["mask"], chunk=e["chunk"]) == e["chunk_areas"]
+        got = P.debug_eval("demands", mask=e["mask"], chunk=e["chunk"], cp=e["cp"],
+                           assignment=e["assignment"])
+        assert got["demands"] == e["demands"]
+        assert got["cast"] == e["cast"]
+        assert got["reduce"] == e["reduce"]
+        assert got["redundancy"] == e["redundancy"]
+
+
+def test_overlap_pieces(P):
+    for tr, mn, mx, want in GOLD["partition_packages"]:
+        assert P.debug_eval("partition_packages", traffic=tr, min=mn, max=mx) == want
+    for e in GOLD["assign_packages"]:
+        assert P.debug_eval("assign_packages", sizes=e["sizes"], stages=e["stages"]) == e["lpt"]
+        if "seed" in e:
+            got = P.debug_eval("assign_packages", sizes=e["sizes"], stages=e["stages"], seed=e["seed"])
+            assert got == e["shuffled"]
+    for e in GOLD["estimates"]:
+        assert P.debug_eval("estimate", host=e["host"], compute=e["compute"], cast=e["cast"],
+                            reduce=e["reduce"]) == [e["fwd"], e["bwd"]]
+    for e in GOLD["fit_affine"]:
+        assert P.debug_eval("fit_affine", samples=e["samples"]) == pytest.approx(e["fit"], rel=0, abs=0)
+
+
+def test_lognormal_lengths(P):
+    assert P.lognormal_lengths(200, 2048.0, 1.0, 65536, 42) == GOLD["lognormal_2048_1.0_65536_seed42"]
+
+
+def test_flops(P):
+    got = P.debug_eval("flops", mask={"seqlen": 4096, "pattern": "full"}, num_heads_q=64, head_dim=128)
+    assert got == GOLD["flops_full4096_h64_d128"] == [549755813888, 1374389534720]
+
+
+@pytest.mark.parametrize("idx", range(len(GOLD["scenarios"])))
+def test_scenarios_byte_identical(P, idx):
+    from paper_2505_13211_b200 import _lib
+
+    e = GOLD["scenarios"][idx]
+    text = e["scenario"]
+    try:
+        sc = P.Scenario(text)
+    except _lib.MagiplanError as err:
+        assert e.get("plan", "").startswith("ERROR") or e.get("simulate", "").startswith("ERROR")
+        want = (e.get("plan") or e["simulate"])[len("ERROR "):]
+        assert err.message == want
+        return
+    if "plan" in e:
+        if e["plan"].startswith("ERROR"):
+            with pytest.raises(_lib.MagiplanError) as ei:
+                sc.plan_text()
+            assert ei.value.message == e["plan"][len("ERROR "):]
+        else:
+            assert sc.plan_text() == e["plan"]
+    if "simulate" in e and '"schedule": "ring"' not in text:
+        if e["simulate"].startswith("ERROR"):
+            with pytest.raises(_lib.MagiplanError):
+                sc.simulate_text(2)
+        else:
+            assert sc.simulate_text(2) == e["simulate"]
