@@ -1,0 +1,141 @@
+"""C ABI boundary (CPU): exports, status mapping, error text, ownership.
+
+Mirrors the reference's C ABI suite (proj/tests/test_capi.cpp:52-228):
+status codes 2/3/4, thread-local last_error, byte-identical reruns across
+jobs=1/2, and plan/simulate agreement."""
+import ctypes as C
+import json
+import re
+import threading
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols() -> list[str]:
+    text = (ROOT / "include" / "magiplan.h").read_text()
+    return re.findall(r"MAGIPLAN_API\s+[\w\s\*]+?\b(magiplan_\w+)\s*\(", text)
+
+
+def test_every_declared_symbol_is_exported(built_lib):
+    from paper_2505_13211_b200 import _lib
+
+    names = declared_symbols()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(built_lib, n)]
+    assert not missing, missing
+    # the 14 reference entry points (magiplan.h:61-121) are all present
+    ref14 = ["magiplan_version", "magiplan_last_error", "magiplan_string_free", "magiplan_mask_parse",
+             "magiplan_mask_free", "magiplan_mask_area", "magiplan_mask_is_allowed",
+             "magiplan_mask_render", "magiplan_mask_describe", "magiplan_scenario_parse",
+             "magiplan_scenario_free", "magiplan_scenario_set_seed", "magiplan_scenario_plan",
+             "magiplan_scenario_simulate", "magiplan_pack_run"]
+    assert set(ref14) <= set(names)
+    assert set(names) <= set(_lib.SIGNATURES), set(names) - set(_lib.SIGNATURES)
+
+
+def test_version_and_status_mapping(built_lib):
+    from paper_2505_13211_b200 import _lib
+
+    L = built_lib
+    assert L.magiplan_version() == b"0.1.0"
+    h = C.c_void_p()
+    assert L.magiplan_mask_parse(None, C.byref(h)) == _lib.ERR_USAGE
+    assert L.magiplan_last_error() == b"null argument"
+    assert L.magiplan_mask_parse(b"{not json", C.byref(h)) == _lib.ERR_USAGE
+    assert b"mask spec" in L.magiplan_last_error()
+    assert h.value is None  # outputs untouched on failure
+    st = L.magiplan_mask_parse(b'{"seqlen": 10, "pattern": "block_causal", "params": {"block_size": 3}}',
+                               C.byref(h))
+    assert st == _lib.ERR_CONSTRAINT and b"does not divide" in L.magiplan_last_error()
+    assert L.magiplan_mask_parse(b'{"seqlen": 8, "pattern": "causal"}', C.byref(h)) == _lib.OK
+    assert L.magiplan_last_error() == b""  # success clears the error
+    area = C.c_int64()
+    assert L.magiplan_mask_area(h, _lib.COUNT_UNION, C.byref(area)) == _lib.OK and area.value == 36
+    ok = C.c_int()
+    assert L.magiplan_mask_is_allowed(h, 8, 0, C.byref(ok)) == _lib.ERR_USAGE
+    L.magiplan_mask_free(h)
+
+
+def test_last_error_is_thread_local(built_lib):
+    from paper_2505_13211_b200 import _lib
+
+    L = built_lib
+    h = C.c_void_p()
+    assert L.magiplan_mask_parse(b"[]", C.byref(h)) == _lib.ERR_USAGE
+    seen = {}
+
+    def other():
+        seen["err"] = L.magiplan_last_error()
+
+    t = threading.Thread(target=other)
+    t.start()
+    t.join()
+    assert seen["err"] == b""
+    assert L.magiplan_last_error() != b""
+
+
+def test_scenario_reruns_identical_and_jobs_invariant(built_lib):
+    from paper_2505_13211_b200.planner import Scenario
+
+    spec = {"workload": {"mask": {"seqlen": 8192, "pattern": "full"}, "num_heads_q": 8},
+            "sweep": {"cp_sizes": [1, 2, 4, 8], "per_rank_seqlen": 4096},
+            "cost_model": {"ffa_fwd": {"latency": 1, "per_unit": 1e-4},
+                           "cast": {"latency": 5, "per_unit": 0.01},
+                           "reduce": {"latency": 5, "per_unit": 0.01},
+                           "ffa_bwd": {"latency": 1, "per_unit": 2.5e-4}}}
+    sc = Scenario(spec)
+    a, b = sc.simulate_text(1), sc.simulate_text(2)
+    assert a == b and len(a.strip().splitlines()) == 8
+    sc.set_seed(9)
+    assert all(json.loads(l)["seed"] == 9 for l in sc.simulate_text(1).splitlines())
+
+
+def test_plan_and_simulate_agree(built_lib):
+    """estimate == simulated makespan (reference test_sim.cpp:140-181)."""
+    from paper_2505_13211_b200.planner import Scenario
+
+    spec = {"workload": {"mask": {"seqlen": 16384, "pattern": "block_causal",
+                                  "params": {"block_size": 2048}}},
+            "cp_size": 4,
+            "cost_model": {"ffa_fwd": {"latency": 30, "per_unit": 8.19e-05},
+                           "ffa_bwd": {"latency": 30, "per_unit": 2.05e-04},
+                           "cast": {"latency": 100, "per_unit": 0.082},
+                           "reduce": {"latency": 100, "per_unit": 0.082}}}
+    sc = Scenario(spec)
+    plan = sc.plan()
+    fwd, bwd = (json.loads(l) for l in sc.simulate_text().splitlines())
+    est_f = max(r["est_cost_fwd"] for r in plan["overlap"]["ranks"])
+    est_b = max(r["est_cost_bwd"] for r in plan["overlap"]["ranks"])
+    assert fwd["makespan"] == est_f and bwd["makespan"] == est_b
+
+
+def test_out_of_scope_entry_points_fail_loudly(built_lib):
+    from paper_2505_13211_b200 import _lib
+
+    out = C.c_void_p()
+    assert built_lib.magiplan_pack_run(b"{}", None, C.byref(out)) == _lib.ERR_USAGE
+    assert b"out of scope" in built_lib.magiplan_last_error()
+    from paper_2505_13211_b200.planner import Scenario
+
+    sc = Scenario({"workload": {"mask": {"seqlen": 64, "pattern": "causal"}}, "cp_size": 2,
+                   "schedule": "ulysses"})
+    with pytest.raises(_lib.UsageError):
+        sc.simulate_text()
+
+
+def test_ffa_plan_validation_on_cpu(built_lib):
+    """Plan construction is host-only until upload; bad slices are USAGE errors."""
+    from paper_2505_13211_b200 import _lib
+
+    L = built_lib
+    qr = (C.c_int64 * 2)(0, 300)
+    kr = (C.c_int64 * 2)(0, 100)
+    ty = (C.c_int32 * 1)(0)
+    h = C.c_void_p()
+    st = L.magiplan_ffa_plan_create(qr, kr, ty, 1, 200, 200, 128, C.byref(h))
+    assert st == _lib.ERR_USAGE and b"exceeds mask bounds" in L.magiplan_last_error()
+    st = L.magiplan_ffa_plan_create(qr, kr, ty, 1, 300, 300, 96, C.byref(h))
+    assert st == _lib.ERR_USAGE and b"head_dim" in L.magiplan_last_error()
