@@ -1,0 +1,288 @@
+"""Context-parallel FFA executor: dispatch + GroupCast / GroupReduce + staged
+FFA with overlap, one process per GPU over torch.distributed (NCCL).
+
+This is the real counterpart of the reference's ``simulate_magi`` schedule
+(/root/reference/proj/src/sim.cpp:174-259): the plan (dispatch,
+zero-redundant transfer tables, stage split) comes from the planner through
+``magiplan_scenario_exec_plan``; every stage is executed with the sm_100a
+FFA kernels; communication runs on its own CUDA streams.
+
+Forward, per rank (§4.2, Alg. 2):
+    step 0      FFA(local Q, local KV)                 || GroupCast(stage 1)
+    step j      FFA(local Q, stage-j KV), LSE merge    || GroupCast(stage j+1)
+Backward:
+    step 0      dQ, dK, dV from local KV                || GroupCast(stage 1)
+    step j      dQ += ..., partial dK/dV of stage j     || GroupCast(j+1) || GroupReduce(j-1)
+    final       GroupReduce(last stage)
+GroupCast = range-gather kernel + NCCL all_to_all_single (grouped by source
+rank, which is the receive-buffer layout the planner emits). GroupReduce =
+the transposed all-to-all of f32 partial dK/dV followed by the deterministic
+range scatter-add kernel, one source rank at a time in rank order.
+"""
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .ffa import FFAPlan
+from .planner import Scenario
+
+
+@dataclass
+class StageLayout:
+    """Communication + compute layout of one stage on one rank."""
+
+    buf_tokens: int
+    recv_splits: list[int]                 # tokens received from each source rank
+    send_splits: list[int]                 # tokens sent to each destination rank
+    send_ranges: list[tuple[int, int]]     # local [start, end) rows, send-buffer order
+    send_by_dst: list[list[int]]           # indices into send_ranges per destination
+    slices: list[list[int]]                # [qs, qe, ks, ke, type] local q / buffer k
+    plan: FFAPlan | None = None
+    dev: dict = field(default_factory=dict)
+
+
+def _stage_layouts(xplan: dict, rank: int, key: str) -> list[StageLayout]:
+    cp = xplan["cp_size"]
+    ranks = xplan["ranks"]
+    n = max(len(r[key]) for r in ranks)
+    out = []
+    for j in range(n):
+        mine = ranks[rank][key][j] if j < len(ranks[rank][key]) else {"buf_tokens": 0, "recv": [], "slices": []}
+        recv_splits = [0] * cp
+        for src, gs, ge, _sl, _off in mine["recv"]:
+            recv_splits[src] += ge - gs
+        send_splits = [0] * cp
+        send_ranges: list[tuple[int, int]] = []
+        send_by_dst: list[list[int]] = [[] for _ in range(cp)]
+        for dst in range(cp):
+            st = ranks[dst][key][j] if j < len(ranks[dst][key]) else None
+            if st is None:
+                continue
+            for src, gs, ge, src_local, _off in st["recv"]:
+                if src != rank:
+                    continue
+                send_by_dst[dst].append(len(send_ranges))
+                send_ranges.append((src_local, src_local + (ge - gs)))
+                send_splits[dst] += ge - gs
+        out.append(StageLayout(mine["buf_tokens"], recv_splits, send_splits, send_ranges,
+                               send_by_dst, mine["slices"]))
+    return out
+
+
+def _ranges_tensor(ranges: list[tuple[int, int]], device) -> tuple[torch.Tensor, torch.Tensor]:
+    r = torch.tensor(ranges if ranges else [[0, 0]], dtype=torch.int64).reshape(-1, 2)
+    lens = (r[:, 1] - r[:, 0]).tolist() if ranges else [0]
+    offs = [0]
+    for x in lens[:-1]:
+        offs.append(offs[-1] + x)
+    return r.to(device), torch.tensor(offs, dtype=torch.int64, device=device)
+
+
+class CPAttention:
+    """Context-parallel FFA over one scenario (mask + dispatch + stages).
+
+    Every rank builds the same executor plan from the same scenario (the
+    planner is deterministic), then keeps only its own view.
+    """
+
+    def __init__(self, scenario: dict | str, num_heads_q: int, num_heads_k: int, head_dim: int,
+                 group=None, device=None, softmax_scale: float | None = None):
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.hq, self.hk, self.d = num_heads_q, num_heads_k, head_dim
+        self.scale = 1.0 / math.sqrt(head_dim) if softmax_scale is None else softmax_scale
+        self.xplan = Scenario(scenario).exec_plan()
+        if self.xplan["cp_size"] != self.world:
+            raise ValueError(f"scenario cp_size {self.xplan['cp_size']} != world size {self.world}")
+        me = self.xplan["ranks"][self.rank]
+        self.chunks = me["chunks"]
+        self.chunk_size = self.xplan["chunk_size"]
+        self.local_tokens = self.xplan["local_tokens"]
+        L = self.local_tokens
+        hs = me["host_slices"]
+        self.host_plan = FFAPlan([s[0:2] for s in hs], [s[2:4] for s in hs], [s[4] for s in hs], L, L,
+                                 head_dim) if hs else None
+        self.fwd_stages = _stage_layouts(self.xplan, self.rank, "fwd_stages")
+        self.bwd_stages = _stage_layouts(self.xplan, self.rank, "bwd_stages")
+        for st in self.fwd_stages + self.bwd_stages:
+            if st.slices:
+                st.plan = FFAPlan([s[0:2] for s in st.slices], [s[2:4] for s in st.slices],
+                                  [s[4] for s in st.slices], L, st.buf_tokens, head_dim)
+            st.dev["send"] = _ranges_tensor(st.send_ranges, self.device)
+            per_dst = []
+            for dst in range(self.world):
+                rr = [st.send_ranges[i] for i in st.send_by_dst[dst]]
+                per_dst.append(_ranges_tensor(rr, self.device) + (sum(b - a for a, b in rr),))
+            st.dev["per_dst"] = per_dst
+        self.comm_stream = torch.cuda.Stream(self.device)
+        self.reduce_stream = torch.cuda.Stream(self.device)
+        self.L = _lib.lib()
+
+    # ------------------------------------------------------------ data layout
+    def local_token_index(self) -> torch.Tensor:
+        """Global token ids of this rank's local rows (chunk order)."""
+        cs = self.chunk_size
+        idx = [torch.arange(c * cs, (c + 1) * cs) for c in self.chunks]
+        return torch.cat(idx) if idx else torch.empty(0, dtype=torch.int64)
+
+    # ------------------------------------------------------------ primitives
+    def _gather(self, src: torch.Tensor, st: StageLayout, stream) -> torch.Tensor:
+        rows = sum(st.send_splits)
+        out = torch.empty((rows,) + tuple(src.shape[1:]), dtype=src.dtype, device=src.device)
+        if rows:
+            ranges, offs = st.dev["send"]
+            row_bytes = src[0].numel() * src.element_size()
+            _lib.check(self.L.magiplan_range_gather(src.data_ptr(), out.data_ptr(), ranges.data_ptr(),
+                                                    offs.data_ptr(), len(st.send_ranges), rows,
+                                                    row_bytes, stream.cuda_stream))
+        return out
+
+    def _cast(self, st: StageLayout, k: torch.Tensor, v: torch.Tensor):
+        """GroupCast of stage `st` on the comm stream; returns (k_buf, v_buf, works)."""
+        with torch.cuda.stream(self.comm_stream):
+            ks = self._gather(k, st, self.comm_stream)
+            vs = self._gather(v, st, self.comm_stream)
+            kb = torch.empty((st.buf_tokens, self.hk, self.d), dtype=k.dtype, device=k.device)
+            vb = torch.empty_like(kb)
+            works = []
+            if self.world > 1:
+                works.append(dist.all_to_all_single(kb, ks, st.recv_splits, st.send_splits,
+                                                    group=self.group, async_op=True))
+                works.append(dist.all_to_all_single(vb, vs, st.recv_splits, st.send_splits,
+                                                    group=self.group, async_op=True))
+        return kb, vb, works, (ks, vs)
+
+    def _reduce(self, st: StageLayout, dk_buf, dv_buf, dk, dv):
+        """GroupReduce of a stage's f32 partial dK/dV into the hosts' dK/dV."""
+        with torch.cuda.stream(self.reduce_stream):
+            rows = sum(st.send_splits)
+            rk = torch.empty((rows, self.hk, self.d), dtype=torch.float32, device=dk.device)
+            rv = torch.empty_like(rk)
+            if self.world > 1:
+                dist.all_to_all_single(rk, dk_buf, st.send_splits, st.recv_splits, group=self.group)
+                dist.all_to_all_single(rv, dv_buf, st.send_splits, st.recv_splits, group=self.group)
+            base = 0
+            row_elems = self.hk * self.d
+            for dst in range(self.world):  # fixed source-rank order => deterministic sums
+                ranges, offs, n = st.dev["per_dst"][dst]
+                if n:
+                    sp = self.reduce_stream.cuda_stream
+                    for part, acc in ((rk, dk), (rv, dv)):
+                        _lib.check(self.L.magiplan_range_scatter_add_f32(
+                            part[base:].data_ptr(), acc.data_ptr(), ranges.data_ptr(), offs.data_ptr(),
+                            len(st.send_by_dst[dst]), n, row_elems, sp))
+                base += n
+        return rk, rv
+
+    # ------------------------------------------------------------ forward
+    def forward(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor):
+        """q: [L, hq, d], k/v: [L, hk, d] bf16 local shards (chunk order).
+        Returns (out bf16 [L, hq, d], lse f32 [hq, L], out f32 for backward)."""
+        from .ffa import ffa_forward
+
+        L = self.local_tokens
+        out = torch.empty((L, self.hq, self.d), dtype=torch.float32, device=q.device)
+        lse = torch.empty((self.hq, L), dtype=torch.float32, device=q.device)
+        cur = torch.cuda.current_stream(q.device)
+        self.comm_stream.wait_stream(cur)
+        pending = self._cast(self.fwd_stages[0], k, v) if self.fwd_stages else None
+        if self.host_plan is not None:
+            ffa_forward(self.host_plan, q, k, v, self.scale, out=out, lse=lse)
+        else:
+            out.zero_()
+            lse.fill_(-math.inf)
+        for j, st in enumerate(self.fwd_stages):
+            kb, vb, works, keep = pending
+            if j + 1 < len(self.fwd_stages):
+                pending = self._cast(self.fwd_stages[j + 1], k, v)
+            for w in works:
+                w.wait()
+            cur.wait_stream(self.comm_stream)
+            if st.plan is not None:
+                ffa_forward(st.plan, q, kb, vb, self.scale, out=out, lse=lse, accumulate=True)
+            kb.record_stream(cur)
+            vb.record_stream(cur)
+        out_bf = torch.empty((L, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
+        _lib.check(self.L.magiplan_cast_f32_bf16(out.data_ptr(), out_bf.data_ptr(), out.numel(),
+                                                 cur.cuda_stream))
+        return out_bf, lse, out
+
+    # ------------------------------------------------------------ backward
+    def backward(self, q, k, v, out_f32, lse, dout):
+        """Returns (dq, dk, dv) bf16 local shards."""
+        from .ffa import ffa_backward
+
+        L = self.local_tokens
+        dev = q.device
+        cur = torch.cuda.current_stream(dev)
+        sp = cur.cuda_stream
+        delta = torch.empty((self.hq, L), dtype=torch.float32, device=dev)
+        _lib.check(self.L.magiplan_ffa_bwd_preprocess(out_f32.data_ptr(), dout.data_ptr(),
+                                                      delta.data_ptr(), L, self.hq, self.d, _lib.F32, sp))
+        dq = torch.empty((L, self.hq, self.d), dtype=torch.float32, device=dev)
+        dk = torch.empty((L, self.hk, self.d), dtype=torch.float32, device=dev)
+        dv = torch.empty_like(dk)
+        self.comm_stream.wait_stream(cur)
+        pending = self._cast(self.bwd_stages[0], k, v) if self.bwd_stages else None
+        if self.host_plan is not None:
+            ffa_backward(self.host_plan, q, k, v, out_f32, lse, dout, self.scale, delta=delta,
+                         dq=dq, dk=dk, dv=dv)
+        else:
+            dq.zero_()
+            dk.zero_()
+            dv.zero_()
+        self.reduce_stream.wait_stream(cur)  # dk/dv initialised before any scatter-add
+        keep = []
+        for j, st in enumerate(self.bwd_stages):
+            kb, vb, works, sent = pending
+            if j + 1 < len(self.bwd_stages):
+                pending = self._cast(self.bwd_stages[j + 1], k, v)
+            for w in works:
+                w.wait()
+            cur.wait_stream(self.comm_stream)
+            dkb = torch.zeros((st.buf_tokens, self.hk, self.d), dtype=torch.float32, device=dev)
+            dvb = torch.zeros_like(dkb)
+            if st.plan is not None:
+                Ld = self.L
+                _lib.check(Ld.magiplan_ffa_bwd_dq(st.plan.handle, q.data_ptr(), kb.data_ptr(),
+                                                  vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                                  dout.data_ptr(), dq.data_ptr(), self.hq, self.hk,
+                                                  self.scale, _lib.F32, 1, sp))
+                _lib.check(Ld.magiplan_ffa_bwd_dkdv(st.plan.handle, q.data_ptr(), kb.data_ptr(),
+                                                    vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                                    dout.data_ptr(), dkb.data_ptr(), dvb.data_ptr(),
+                                                    self.hq, self.hk, self.scale, _lib.F32, 0, sp))
+            kb.record_stream(cur)
+            vb.record_stream(cur)
+            self.reduce_stream.wait_stream(cur)
+            keep.append(self._reduce(st, dkb, dvb, dk, dv))
+            dkb.record_stream(self.reduce_stream)
+            dvb.record_stream(self.reduce_stream)
+        cur.wait_stream(self.reduce_stream)
+        outs = []
+        for t in (dq, dk, dv):
+            b = torch.empty(t.shape, dtype=torch.bfloat16, device=dev)
+            _lib.check(self.L.magiplan_cast_f32_bf16(t.data_ptr(), b.data_ptr(), t.numel(), sp))
+            outs.append(b)
+        del keep
+        return tuple(outs)
+
+    # ------------------------------------------------------------ accounting
+    def flops(self) -> tuple[int, int]:
+        """Whole-job mask-aware FLOPs (fwd, bwd), reference sim.cpp:29-34."""
+        fwd = 4 * int(self.xplan["area_multiplicity"]) * self.hq * self.d
+        return fwd, fwd * 5 // 2
+
+    def comm_tokens(self) -> dict:
+        cast = sum(sum(st.recv_splits) for st in self.fwd_stages)
+        return {"fwd_cast_recv_tokens": cast,
+                "bwd_cast_recv_tokens": sum(sum(st.recv_splits) for st in self.bwd_stages),
+                "bwd_reduce_recv_tokens": sum(sum(st.send_splits) for st in self.bwd_stages)}

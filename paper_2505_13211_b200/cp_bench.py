@@ -1,0 +1,143 @@
+"""Multi-GPU leg of bench.py: context-parallel FFA fwd+bwd, weak scaling.
+
+Workload: MAGI-1 24B attention shape (48 query
+heads, 8 key/value heads, head_dim 128), block-causal with block 8192,
+131072 tokens per rank (N=8 is the 1M-token sequence), greedy dispatch with
+the default chunk (S/cp/8), GroupCast/GroupReduce over NCCL, stage count
+from the overlap solver. `value` = whole-job mask-aware TFLOPS = total FLOPs
+/ max-over-ranks device time.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+
+import torch
+import torch.distributed as dist
+
+PER_RANK = 131072
+HQ, HK, D, BLOCK = 48, 8, 128, 8192
+# B200 cost model for the overlap solver: ~800 TFLOPS FFA, ~300 GB/s effective cast
+COST = {"ffa_fwd": {"latency": 20, "per_unit": 4 * HQ * D / 8.0e8},
+        "ffa_bwd": {"latency": 20, "per_unit": 10 * HQ * D / 6.0e8},
+        "cast": {"latency": 30, "per_unit": (2 * HK * D * 2) / 3.0e5},
+        "reduce": {"latency": 30, "per_unit": (2 * HK * D * 4) / 3.0e5}}
+
+
+def scenario(cp: int) -> dict:
+    S = PER_RANK * cp
+    return {"workload": {"mask": {"seqlen": S, "pattern": "block_causal", "params": {"block_size": BLOCK}},
+                         "num_heads_q": HQ, "num_heads_k": HK, "num_heads_v": HK, "head_dim": D},
+            "cp_size": cp, "cost_model": COST,
+            "overlap": {"min_chunk_size": 4096, "max_num_chunks": 8}}
+
+
+def run(args) -> None:
+    from bench import METRIC, UNIT, ClockSampler, _peaks
+    from paper_2505_13211_b200.cp import CPAttention
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cpa = CPAttention(scenario(world), HQ, HK, D)
+    L = cpa.local_tokens
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    q_h = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).pin_memory()
+    k_h = torch.randn(L, HK, D, generator=g).to(torch.bfloat16).pin_memory()
+    v_h = torch.randn(L, HK, D, generator=g).to(torch.bfloat16).pin_memory()
+    do_h = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).pin_memory()
+    q, k, v, do = (t.to(dev) for t in (q_h, k_h, v_h, do_h))
+
+    def step():
+        out, lse, out32 = cpa.forward(q, k, v)
+        return cpa.backward(q, k, v, out32, lse, do)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+
+    # e2e: host buffers in, gradients out, every step
+    dq_h = torch.empty(L, HQ, D, dtype=torch.bfloat16).pin_memory()
+    dk_h = torch.empty(L, HK, D, dtype=torch.bfloat16).pin_memory()
+    dv_h = torch.empty(L, HK, D, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        for dst, src in ((q, q_h), (k, k_h), (v, v_h), (do, do_h)):
+            dst.copy_(src, non_blocking=True)
+        dq, dk, dv = step()
+        dq_h.copy_(dq, non_blocking=True)
+        dk_h.copy_(dk, non_blocking=True)
+        dv_h.copy_(dv, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 3))
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], device=dev)
+    dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    clk = clocks.stop() if rank == 0 else None
+
+    fwd, bwd = cpa.flops()
+    total = fwd + bwd
+    comm = torch.tensor([list(cpa.comm_tokens().values())], dtype=torch.float64, device=dev)
+    dist.all_reduce(comm)
+    if rank == 0:
+        peaks = _peaks()
+        value = total / (ms.item() * 1e-3) / 1e12
+        per_gpu = value / world
+        n_launch = 0
+        for st in cpa.fwd_stages:
+            n_launch += 1 + 2 * (1 if sum(st.send_splits) else 0)
+        for st in cpa.bwd_stages:
+            n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
+        n_launch += 2 + 1 + 2 + 3  # host fwd + cast, preprocess, host bwd (2), final casts
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms.item(), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": "cp_block_causal_magi1_24b", "seqlen": PER_RANK * world,
+                       "tokens_per_rank": PER_RANK, "num_heads_q": HQ, "num_heads_k": HK, "head_dim": D,
+                       "mask": f"block_causal(block={BLOCK})", "dispatch": "greedy",
+                       "dispatch_chunk_size": cpa.chunk_size, "num_stages_fwd": cpa.xplan["num_stages_fwd"],
+                       "num_stages_bwd": cpa.xplan["num_stages_bwd"], "parallelism": f"cp{world}",
+                       "flops_per_step": total,
+                       "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),
+                       "comm_tokens_all_ranks": dict(zip(cpa.comm_tokens().keys(), comm[0].tolist())),
+                       "l2": "inputs larger than L2 per rank; no flush"},
+            "roofline": {"bound": "tensor", "kernel": "whole CP step", "achieved": per_gpu,
+                         "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": per_gpu / peaks["bf16"],
+                         "traffic": None, "peak_source": peaks["source"]},
+            "tflops_per_gpu": per_gpu,
+            "e2e": {"value": total / (e2e_ms.item() * 1e-3) / 1e12, "unit": UNIT,
+                    "h2d_bytes_per_step": sum(t.numel() * 2 for t in (q_h, k_h, v_h, do_h)),
+                    "d2h_bytes_per_step": sum(t.numel() * 2 for t in (dq_h, dk_h, dv_h)),
+                    "ms_per_step": e2e_ms.item(), "per_rank": True},
+            "clocks": clk,
+            "gpu_launches": n_launch * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

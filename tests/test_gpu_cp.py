@@ -1,0 +1,102 @@
+"""Context-parallel FFA on >= 2 GPUs (NCCL), checked against the CPU oracle
+on the global sequence. Tolerances as tests/test_gpu_ffa_bwd.py (bf16
+outputs: max abs error <= 4% of max |ref|, LSE <= 1e-3 abs)."""
+import math
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+COST = {"ffa_fwd": {"latency": 30, "per_unit": 8.19e-05}, "ffa_bwd": {"latency": 30, "per_unit": 2.05e-04},
+        "cast": {"latency": 10, "per_unit": 0.0082}, "reduce": {"latency": 10, "per_unit": 0.0082}}
+
+
+def _worker(rank, world, port, mask, chunk, hq, hk, d, outq):
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    try:
+        from paper_2505_13211_b200.cp import CPAttention
+
+        scen = {"workload": {"mask": mask, "num_heads_q": hq, "num_heads_k": hk, "head_dim": d},
+                "cp_size": world, "dispatch_chunk_size": chunk, "cost_model": COST,
+                "overlap": {"min_chunk_size": 128, "max_num_chunks": 4}}
+        cpa = CPAttention(scen, hq, hk, d)
+        S = cpa.xplan["seqlen"]
+        g = torch.Generator().manual_seed(11)
+        Q = torch.randn(S, hq, d, generator=g).to(torch.bfloat16)
+        K = torch.randn(S, hk, d, generator=g).to(torch.bfloat16)
+        V = torch.randn(S, hk, d, generator=g).to(torch.bfloat16)
+        DO = torch.randn(S, hq, d, generator=g).to(torch.bfloat16)
+        idx = cpa.local_token_index()
+        dev = torch.device("cuda", rank)
+        q, k, v, do = (t[idx].contiguous().to(dev) for t in (Q, K, V, DO))
+        out, lse, out32 = cpa.forward(q, k, v)
+        dq, dk, dv = cpa.backward(q, k, v, out32, lse, do)
+        torch.cuda.synchronize()
+        outq.put((rank, idx.numpy(), out.float().cpu().numpy(), lse.cpu().numpy(), dq.float().cpu().numpy(),
+               dk.float().cpu().numpy(), dv.float().cpu().numpy(), cpa.comm_tokens()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mask,chunk", [
+    ({"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 256),
+    ({"seqlen": 2048, "pattern": "varlen_block_causal_last_global",
+      "params": {"sample_lengths": [1024, 512, 512], "block_size": 256}}, 128),
+    ({"seqlen": 3072, "pattern": "causal"}, 192),
+])
+def test_cp_matches_oracle(built_lib, cuda, mask, chunk):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    from oracle import oracle
+    from paper_2505_13211_b200.planner import Mask
+
+    world = min(4, torch.cuda.device_count())
+    hq, hk, d = 4, 2, 128
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    port = 29700 + chunk % 97
+    ps = [ctx.Process(target=_worker, args=(r, world, port, mask, chunk, hq, hk, d, qu)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = [qu.get(timeout=120) for _ in range(world)]
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    m = Mask(mask)
+    S = m.seqlen_q
+    g = torch.Generator().manual_seed(11)
+    Q = torch.randn(S, hq, d, generator=g).to(torch.bfloat16)
+    K = torch.randn(S, hk, d, generator=g).to(torch.bfloat16)
+    V = torch.randn(S, hk, d, generator=g).to(torch.bfloat16)
+    DO = torch.randn(S, hq, d, generator=g).to(torch.bfloat16)
+    qr = [list(s[0]) for s in m.slices]
+    kr = [list(s[1]) for s in m.slices]
+    ty = [s[2] for s in m.slices]
+    scale = 1 / math.sqrt(d)
+    ro, rl = oracle.ffa_fwd(Q, K, V, qr, kr, ty, scale)
+    rdq, rdk, rdv = oracle.ffa_bwd(Q, K, V, ro, rl, DO, qr, kr, ty, scale)
+    out = np.zeros_like(ro)
+    lse = np.zeros_like(rl)
+    dq = np.zeros_like(rdq)
+    dk = np.zeros_like(rdk)
+    dv = np.zeros_like(rdv)
+    for rank, idx, o, l, gq, gk, gv, _ in res:
+        out[idx], lse[:, idx], dq[idx], dk[idx], dv[idx] = o, l, gq, gk, gv
+
+    def rel(a, b):
+        return float(np.abs(a - b).max() / np.abs(b).max())
+
+    assert rel(out, ro) < 4e-2
+    fin = np.isfinite(rl)
+    assert np.abs(lse[fin] - rl[fin]).max() < 1e-3
+    for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        assert rel(got, ref) < 4e-2, rel(got, ref)
