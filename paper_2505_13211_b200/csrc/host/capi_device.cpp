@@ -144,8 +144,8 @@ magiplan_status magiplan_ffa_fwd(const magiplan_ffa_plan* plan, const void* q, c
     check_heads(num_heads_q, num_heads_k);
     check_dtype(out_dtype, accumulate);
     const auto& P = plan->plan;
-    cuda_check(magi::launch_ffa_fwd(P.d_fwd_tiles, P.d_fwd_items,
-                                    static_cast<int>(P.fwd_tiles.size()),
+    cuda_check(magi::launch_ffa_fwd(P.d_fwd2_tiles, P.d_fwd2_items,
+                                    static_cast<int>(P.fwd2_tiles.size()),
                                     static_cast<int>(P.seqlen_q), static_cast<int>(P.seqlen_k),
                                     static_cast<int>(num_heads_q), static_cast<int>(num_heads_k),
                                     P.head_dim, softmax_scale, q, k, v, out, lse,

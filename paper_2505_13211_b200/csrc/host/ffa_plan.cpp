@@ -66,6 +66,8 @@ T* upload(const std::vector<T>& host) {
 FfaPlan::~FfaPlan() {
   cudaFree(d_fwd_tiles);
   cudaFree(d_fwd_items);
+  cudaFree(d_fwd2_tiles);
+  cudaFree(d_fwd2_items);
   cudaFree(d_bwd_tiles);
   cudaFree(d_bwd_items);
 }
@@ -98,6 +100,12 @@ std::string FfaPlan::describe_json() const {
   return j.dump();
 }
 
+namespace {
+void build_qmajor(const FfaPlan& plan, int64_t rows, const std::vector<int>& by_q,
+                  std::vector<magi::FwdTile>& out_tiles, std::vector<magi::FwdItem>& out_items);
+void build_kmajor(FfaPlan& plan);
+}  // namespace
+
 void build_ffa_worklists(FfaPlan& plan) {
   constexpr int64_t kMaxTokens = std::numeric_limits<int32_t>::max() - 2 * kBlockM;
   if (plan.seqlen_q < 0 || plan.seqlen_k < 0) throw UsageError("mask seqlen must be non-negative");
@@ -128,16 +136,27 @@ void build_ffa_worklists(FfaPlan& plan) {
   std::vector<int> by_q(plan.slices.size());
   std::iota(by_q.begin(), by_q.end(), 0);
 
-  // ---- q-major work list
-  plan.fwd_tiles.clear();
-  plan.fwd_items.clear();
-  const int64_t n_qt = ceil_div(plan.seqlen_q, kBlockM);
+  // ---- q-major work lists: 128-row tiles (dQ) and 256-row tiles (forward)
+  build_qmajor(plan, kBlockM, by_q, plan.fwd_tiles, plan.fwd_items);
+  build_qmajor(plan, 2 * kBlockM, by_q, plan.fwd2_tiles, plan.fwd2_items);
+
+  // ---- k-major work list
+  build_kmajor(plan);
+}
+
+namespace {
+
+void build_qmajor(const FfaPlan& plan, int64_t rows, const std::vector<int>& by_q,
+                  std::vector<magi::FwdTile>& out_tiles, std::vector<magi::FwdItem>& out_items) {
+  out_tiles.clear();
+  out_items.clear();
+  const int64_t n_qt = ceil_div(plan.seqlen_q, rows);
   std::vector<magi::FwdTile> tiles;
   tiles.reserve(static_cast<std::size_t>(n_qt));
   std::vector<std::vector<magi::FwdItem>> tile_items(static_cast<std::size_t>(n_qt));
   for (int64_t i = 0; i < n_qt; ++i) {
-    const int64_t q0 = i * kBlockM;
-    const int64_t q1 = std::min<int64_t>(q0 + kBlockM, plan.seqlen_q);
+    const int64_t q0 = i * rows;
+    const int64_t q1 = std::min<int64_t>(q0 + rows, plan.seqlen_q);
     for (int si : by_q) {
       const auto& s = plan.slices[static_cast<std::size_t>(si)];
       if (s.qs >= q1 || s.qe <= q0 || s.ks >= s.ke) continue;
@@ -155,7 +174,7 @@ void build_ffa_worklists(FfaPlan& plan) {
   for (int64_t i = 0; i < n_qt; ++i) {
     int32_t n = 0;
     for (const auto& it : tile_items[static_cast<std::size_t>(i)]) n += it.n_ktiles;
-    tiles.push_back({static_cast<int32_t>(i * kBlockM), 0, 0, n});
+    tiles.push_back({static_cast<int32_t>(i * rows), 0, 0, n});
   }
   std::vector<int64_t> order(static_cast<std::size_t>(n_qt));
   std::iota(order.begin(), order.end(), 0);
@@ -164,13 +183,14 @@ void build_ffa_worklists(FfaPlan& plan) {
   });
   for (int64_t i : order) {
     magi::FwdTile t = tiles[static_cast<std::size_t>(i)];
-    t.item_begin = static_cast<int32_t>(plan.fwd_items.size());
-    for (const auto& it : tile_items[static_cast<std::size_t>(i)]) plan.fwd_items.push_back(it);
-    t.item_end = static_cast<int32_t>(plan.fwd_items.size());
-    plan.fwd_tiles.push_back(t);
+    t.item_begin = static_cast<int32_t>(out_items.size());
+    for (const auto& it : tile_items[static_cast<std::size_t>(i)]) out_items.push_back(it);
+    t.item_end = static_cast<int32_t>(out_items.size());
+    out_tiles.push_back(t);
   }
+}
 
-  // ---- k-major work list
+void build_kmajor(FfaPlan& plan) {
   plan.bwd_tiles.clear();
   plan.bwd_items.clear();
   const int64_t n_kt = ceil_div(plan.seqlen_k, kBlockN);
@@ -234,9 +254,13 @@ void build_ffa_worklists(FfaPlan& plan) {
   }
 }
 
+}  // namespace
+
 void upload_ffa_worklists(FfaPlan& plan) {
   plan.d_fwd_tiles = upload(plan.fwd_tiles);
   plan.d_fwd_items = upload(plan.fwd_items);
+  plan.d_fwd2_tiles = upload(plan.fwd2_tiles);
+  plan.d_fwd2_items = upload(plan.fwd2_items);
   plan.d_bwd_tiles = upload(plan.bwd_tiles);
   plan.d_bwd_items = upload(plan.bwd_items);
 }

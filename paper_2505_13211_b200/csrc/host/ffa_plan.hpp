@@ -17,14 +17,18 @@ struct FfaPlan {
   std::vector<magi::SliceGeom> slices;
   int64_t area_multiplicity = 0;
 
-  std::vector<magi::FwdTile> fwd_tiles;  // LPT order (most key tiles first)
+  std::vector<magi::FwdTile> fwd_tiles;  // 128-row tiles (dQ pass), LPT order
   std::vector<magi::FwdItem> fwd_items;
+  std::vector<magi::FwdTile> fwd2_tiles;  // 256-row tiles (forward), LPT order
+  std::vector<magi::FwdItem> fwd2_items;
   std::vector<magi::BwdTile> bwd_tiles;  // LPT order (most query tiles first)
   std::vector<magi::BwdItem> bwd_items;
 
   // device copies (owned)
   magi::FwdTile* d_fwd_tiles = nullptr;
   magi::FwdItem* d_fwd_items = nullptr;
+  magi::FwdTile* d_fwd2_tiles = nullptr;
+  magi::FwdItem* d_fwd2_items = nullptr;
   magi::BwdTile* d_bwd_tiles = nullptr;
   magi::BwdItem* d_bwd_items = nullptr;
 

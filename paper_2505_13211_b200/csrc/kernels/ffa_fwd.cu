@@ -1,19 +1,28 @@
 // FFA forward for sm_100a: flexible (slice-list) masked attention, O and LSE.
 //
-// One CTA owns one 128-row query tile of one query head and walks every
-// (tile, slice) work item the host planner produced for that tile, so
-// overlapping slices are merged inside the CTA (MULTIPLICITY semantics,
-// reference proj/include/magiplan/mask.hpp:85) with no atomics.
+// One CTA owns a 256-row query tile of one query head, split in two 128-row
+// sub-tiles that share every K/V tile (halving L2 -> SM traffic per FLOP),
+// and walks every (tile, slice) work item the host planner produced for it.
+// Overlapping slices are merged inside the CTA (MULTIPLICITY semantics,
+// reference proj/include/magiplan/mask.hpp:85): no atomics.
 //
-// Warp roles (192 threads):
-//   warps 0-3  softmax: thread i owns query row i of the tile. Reads S from
-//              TMEM (tcgen05.ld 32x32b), applies the per-slice row bounds,
-//              runs the online softmax, rescales O in TMEM, writes P (bf16)
-//              into a 128B-swizzled smem tile, and finally the epilogue.
-//   warp 4     TMA producer: Q once, then K/V tiles through a 2-stage ring.
-//   warp 5     MMA issuer (one lane): S = Q K^T into a double-buffered TMEM
-//              accumulator, O += P V into a TMEM accumulator.
-// TMEM columns: S0 [0,128) S1 [128,256) O [256, 256+D).
+// Warp roles (320 threads):
+//   warps 0-3 / 4-7  softmax of sub-tile 0 / 1: thread = query row = TMEM
+//                    lane. Reads S (tcgen05.ld), applies the slice row bounds,
+//                    online softmax with a lazily moved max (rescale O only
+//                    when the row max grows by > 2^8), exp2 split between MUFU
+//                    and an FMA-pipe polynomial, writes P back into the S
+//                    columns as packed bf16 (tcgen05.st).
+//   warp 8           TMA producer: Q once, K/V through a 2-stage ring.
+//   warp 9           MMA issuer (one lane). Per key tile t:
+//                      S0 = Q0 K^T, S1 = Q1 K^T           (SS, M=128 N=128)
+//                      O0 += P0 V, then S0' = Q0 K'^T      (P from TMEM: TS)
+//                      O1 += P1 V, then S1' = Q1 K'^T
+//                    so softmax of one sub-tile overlaps the MMAs of the other.
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
+// Issue order guarantees: S_i(t+1) is issued after O_i += P_i(t) V, so when a
+// softmax thread sees S_i(t+1) complete, P_i(t)'s MMA has retired and O_i is
+// quiescent until it arrives on p_full — the O rescale needs no extra wait.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -27,10 +36,12 @@ namespace {
 
 constexpr int kStages = 2;
 constexpr uint32_t kBox = 128 * 64 * 2;  // one TMA box: 128 rows x 64 bf16 (128B swizzle)
-constexpr int kSoftmaxThreads = 128;
-constexpr int kThreads = 192;
+constexpr int kSub = 128;                // rows per sub-tile
+constexpr int kTileRows = 2 * kSub;
+constexpr int kThreads = 320;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
+constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 256 between rescales
 
 struct FwdParams {
   const FwdTile* tiles;
@@ -48,21 +59,45 @@ struct FwdParams {
 template <int D>
 struct FwdSmem {
   static constexpr uint32_t kTileBytes = (D / 64) * kBox;
-  static constexpr uint32_t kQ = 0;
-  static constexpr uint32_t kK = kQ + kTileBytes;
+  static constexpr uint32_t kQ = 0;  // 2 sub-tiles
+  static constexpr uint32_t kK = kQ + 2 * kTileBytes;
   static constexpr uint32_t kV = kK + kStages * kTileBytes;
-  static constexpr uint32_t kP = kV + kStages * kTileBytes;
-  static constexpr uint32_t kBytes = kP + 2 * kBox;
+  static constexpr uint32_t kBytes = kV + kStages * kTileBytes;
 };
 
 struct FwdBarriers {
   uint64_t q_full;
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], s_free[2];
-  uint64_t p_full;
-  uint64_t o_done;
+  uint64_t s_full[2], p_full[2], o_final[2];
 };
+
+template <int D>
+__device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint32_t q_addr, uint32_t k_addr) {
+  constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+#pragma unroll
+  for (int k = 0; k < D / 16; ++k) {
+    const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+    umma_bf16_ss(tmem_s, make_smem_desc(q_addr + off, 16, 1024), make_smem_desc(k_addr + off, 16, 1024),
+                 idesc, k > 0);
+  }
+}
+
+template <int D>
+__device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t v_addr,
+                                         bool accumulate) {
+  constexpr uint32_t idesc = make_idesc_bf16(128, D, false, true);
+#pragma unroll
+  for (int k = 0; k < kBlockN / 16; ++k) {
+    umma_bf16_ts(tmem_o, tmem_p + k * 8, make_smem_desc(v_addr + k * 16 * 128, kBox, 1024), idesc,
+                 (accumulate || k > 0) ? 1u : 0u);
+  }
+}
+
+__device__ __forceinline__ void tmem_st16x2(uint32_t taddr, const uint32_t* v) {
+  // 32 consecutive columns from 32 registers
+  tmem_st32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(v));
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -92,36 +127,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars.v_full[s], 1);
       mbar_init(&bars.v_empty[s], 1);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&bars.s_full[b], 1);
-      mbar_init(&bars.s_free[b], kSoftmaxThreads);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars.s_full[i], 1);
+      mbar_init(&bars.p_full[i], kSub);
+      mbar_init(&bars.o_final[i], 1);
     }
-    mbar_init(&bars.p_full, kSoftmaxThreads);
-    mbar_init(&bars.o_done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<512>(&tmem_base_slot);
+  if (warp == 9) tmem_alloc<512>(&tmem_base_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_slot;
-  const uint32_t tmem_s = tmem;        // two 128-column S buffers
-  const uint32_t tmem_o = tmem + 256;  // D columns
 
   uint8_t* sQ = smem + L::kQ;
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
-  uint8_t* sP = smem + L::kP;
 
-  if (warp == 4) {
+  if (warp == 8) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_total > 0) {
       tma_prefetch_desc(&tmap_q);
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
-      mbar_arrive_expect_tx(&bars.q_full, L::kTileBytes);
-      for (int c = 0; c < D / 64; ++c)
-        tma_load_3d(sQ + c * kBox, &tmap_q, &bars.q_full, c * 64, head, tile.q0);
+      mbar_arrive_expect_tx(&bars.q_full, 2 * L::kTileBytes);
+      for (int i = 0; i < 2; ++i)
+        for (int c = 0; c < D / 64; ++c)
+          tma_load_3d(sQ + i * L::kTileBytes + c * kBox, &tmap_q, &bars.q_full, c * 64, head,
+                      tile.q0 + i * kSub);
       PipeState st;
       for (int it = tile.item_begin; it < tile.item_end; ++it) {
         const FwdItem item = p.items[it];
@@ -141,62 +174,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0 && n_total > 0) {
-      constexpr uint32_t idesc_qk = make_idesc_bf16(128, 128, false, false);
-      constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, false, true);
-      const uint32_t q_addr = smem_u32(sQ);
-      const uint32_t p_addr = smem_u32(sP);
+      const uint32_t q_addr0 = smem_u32(sQ), q_addr1 = smem_u32(sQ + L::kTileBytes);
       mbar_wait(&bars.q_full, 0);
-      tc_fence_after();
-
-      auto issue_qk = [&](int t, const PipeState& st) {
-        const int b = t & 1;
-        if (t >= 2) mbar_wait(&bars.s_free[b], ((t - 2) >> 1) & 1);
-        mbar_wait(&bars.k_full[st.index], st.phase);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + st.index * L::kTileBytes);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-          umma_bf16_ss(tmem_s + b * 128, make_smem_desc(q_addr + off, 16, 1024),
-                       make_smem_desc(k_addr + off, 16, 1024), idesc_qk, k > 0);
-        }
-        umma_commit(&bars.s_full[b]);
-        umma_commit(&bars.k_empty[st.index]);
-      };
-
       PipeState kst, vst;
-      issue_qk(0, kst);
-      kst.advance<kStages>();
+      mbar_wait(&bars.k_full[kst.index], kst.phase);
+      tc_fence_after();
+      {
+        const uint32_t k_addr = smem_u32(sK + kst.index * L::kTileBytes);
+        issue_qk<D>(tmem + 0, q_addr0, k_addr);
+        umma_commit(&bars.s_full[0]);
+        issue_qk<D>(tmem + 128, q_addr1, k_addr);
+        umma_commit(&bars.s_full[1]);
+        umma_commit(&bars.k_empty[kst.index]);
+        kst.advance<kStages>();
+      }
       for (int t = 0; t < n_total; ++t) {
-        if (t + 1 < n_total) {
-          issue_qk(t + 1, kst);
-          kst.advance<kStages>();
-        }
-        mbar_wait(&bars.p_full, t & 1);
+        const bool more = t + 1 < n_total;
+        const uint32_t v_addr = smem_u32(sV + vst.index * L::kTileBytes);
+        // sub-tile 0: O0 += P0 V, then S0 for the next key tile
+        mbar_wait(&bars.p_full[0], t & 1);
         mbar_wait(&bars.v_full[vst.index], vst.phase);
         tc_fence_after();
-        const uint32_t v_addr = smem_u32(sV + vst.index * L::kTileBytes);
-#pragma unroll
-        for (int k = 0; k < kBlockN / 16; ++k) {
-          const uint64_t adesc = make_smem_desc(p_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024);
-          const uint64_t bdesc = make_smem_desc(v_addr + k * 16 * 128, kBox, 1024);
-          umma_bf16_ss(tmem_o, adesc, bdesc, idesc_pv, (t > 0 || k > 0) ? 1u : 0u);
+        issue_pv<D>(tmem + 256, tmem + 0, v_addr, t > 0);
+        if (!more) umma_commit(&bars.o_final[0]);
+        uint32_t k_addr = 0;
+        if (more) {
+          mbar_wait(&bars.k_full[kst.index], kst.phase);
+          tc_fence_after();
+          k_addr = smem_u32(sK + kst.index * L::kTileBytes);
+          issue_qk<D>(tmem + 0, q_addr0, k_addr);
+          umma_commit(&bars.s_full[0]);
         }
-        umma_commit(&bars.o_done);
+        // sub-tile 1
+        mbar_wait(&bars.p_full[1], t & 1);
+        tc_fence_after();
+        issue_pv<D>(tmem + 384, tmem + 128, v_addr, t > 0);
         umma_commit(&bars.v_empty[vst.index]);
         vst.advance<kStages>();
+        if (!more) umma_commit(&bars.o_final[1]);
+        if (more) {
+          issue_qk<D>(tmem + 128, q_addr1, k_addr);
+          umma_commit(&bars.s_full[1]);
+          umma_commit(&bars.k_empty[kst.index]);
+          kst.advance<kStages>();
+        }
       }
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int row = warp * 32 + lane;
-    const int q = tile.q0 + row;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
-    float m = -INFINITY;  // running max, log2 domain
-    float l = 0.f;        // running sum of 2^(x - m)
+    const int sub = warp / 4;
+    const int row = (warp % 4) * 32 + lane;
+    const int q = tile.q0 + sub * kSub + row;
+    const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
+    const uint32_t t_s = tmem + sub * 128 + lane_off;
+    const uint32_t t_o = tmem + 256 + sub * 128 + lane_off;
+    const float sl2 = p.scale_log2;
+    float m = -INFINITY;  // exponent base, log2 domain (lazily moved)
+    float l = 0.f;        // sum of 2^(x - m)
     int t = 0;
     for (int it = tile.item_begin; it < tile.item_end; ++it) {
       const FwdItem item = p.items[it];
@@ -204,77 +241,75 @@ __global__ void __launch_bounds__(kThreads, 1)
       row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q, lo, hi);
       for (int j = 0; j < item.n_ktiles; ++j, ++t) {
         const int k0 = item.k_begin + j * kBlockN;
-        const int b = t & 1;
-        mbar_wait(&bars.s_full[b], (t >> 1) & 1);
+        mbar_wait(&bars.s_full[sub], t & 1);
         tc_fence_after();
         uint32_t s[128];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
-          tmem_ld32(tmem_s + lane_off + b * 128 + c * 32, chunk);
+          tmem_ld32(t_s + c * 32, chunk);
         }
         tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&bars.s_free[b]);
 
-        float x[128];
-        float mt = -INFINITY;
         const bool full = lo <= k0 && k0 + kBlockN <= hi;
+        float mt = -INFINITY;
         if (full) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) {
-            x[i] = __uint_as_float(s[i]) * p.scale_log2;
-            mt = fmaxf(mt, x[i]);
-          }
+          for (int i = 0; i < 128; ++i) mt = fmaxf(mt, __uint_as_float(s[i]));
         } else {
 #pragma unroll
           for (int i = 0; i < 128; ++i) {
             const int c = k0 + i;
-            x[i] = (c >= lo && c < hi) ? __uint_as_float(s[i]) * p.scale_log2 : -INFINITY;
-            mt = fmaxf(mt, x[i]);
+            const float v = (c >= lo && c < hi) ? __uint_as_float(s[i]) : -INFINITY;
+            s[i] = __float_as_uint(v);
+            mt = fmaxf(mt, v);
           }
         }
-        const float m_new = fmaxf(m, mt);
-        const float m_use = m_new == -INFINITY ? 0.f : m_new;
-        const float alpha = fast_exp2(m - m_use);
+        const float mt2 = mt * sl2;
+        const bool move = mt2 > m + kRescaleThreshold;  // also true on the first finite tile
+        const float alpha = move ? fast_exp2(m - mt2) : 1.f;
+        if (move) m = mt2;
+        const float mb = m == -INFINITY ? 0.f : m;
         float rs = 0.f;
+        uint32_t pk[64];
+        if (full) {
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          x[i] = fast_exp2(x[i] - m_use);
-          rs += x[i];
+          for (int i = 0; i < 128; i += 2) {
+            const float x0 = fmaf(__uint_as_float(s[i]), sl2, -mb);
+            const float x1 = fmaf(__uint_as_float(s[i + 1]), sl2, -mb);
+            // every 4th element on the FMA pipe: MUFU ex2 is 1/8 of FMA throughput
+            const float p0 = fast_exp2(x0);
+            const float p1 = (i % 4 == 2) ? exp2_poly(x1) : fast_exp2(x1);
+            rs += p0 + p1;
+            pk[i / 2] = pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 128; i += 2) {
+            const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
+            rs += p0 + p1;
+            pk[i / 2] = pack_bf16(p0, p1);
+          }
         }
         l = l * alpha + rs;
-        m = m_new;
-
-        // P buffer and O are owned by the previous PV MMA until it retires.
-        if (t > 0) {
-          mbar_wait(&bars.o_done, (t - 1) & 1);
-          tc_fence_after();
-          if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        // P (bf16 pairs) into the first 64 columns of this sub-tile's S
+        tmem_st16x2(t_s, &pk[0]);
+        tmem_st16x2(t_s + 32, &pk[32]);
+        if (t > 0 && __any_sync(0xffffffffu, move)) {
 #pragma unroll 1
-            for (int c = 0; c < D / 32; ++c) {
-              uint32_t o[32];
-              tmem_ld32(tmem_o + lane_off + c * 32, o);
-              tmem_ld_wait();
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c * 32, o);
+            tmem_ld_wait();
 #pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-              tmem_st32(tmem_o + lane_off + c * 32, o);
-            }
-            tmem_st_wait();
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st32(t_o + c * 32, o);
           }
         }
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          uint4 v;
-          v.x = pack_bf16(x[c * 8 + 0], x[c * 8 + 1]);
-          v.y = pack_bf16(x[c * 8 + 2], x[c * 8 + 3]);
-          v.z = pack_bf16(x[c * 8 + 4], x[c * 8 + 5]);
-          v.w = pack_bf16(x[c * 8 + 6], x[c * 8 + 7]);
-          *reinterpret_cast<uint4*>(sP + (c / 8) * kBox + sw128_offset(row, c % 8)) = v;
-        }
-        fence_proxy_async_smem();
+        tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&bars.p_full);
+        mbar_arrive(&bars.p_full[sub]);
       }
     }
 
@@ -284,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float lse_cur = has ? (m * kLn2 + logf(l)) : -INFINITY;
     const float inv_l = has ? 1.f / l : 0.f;
     if (n_total > 0) {
-      mbar_wait(&bars.o_done, (n_total - 1) & 1);
+      mbar_wait(&bars.o_final[sub], 0);
       tc_fence_after();
     }
     const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D;
@@ -300,8 +335,10 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
-        tmem_ld32(tmem_o + lane_off + c * 32, o);
-        tmem_ld_wait();
+        if (n_total > 0) {
+          tmem_ld32(t_o + c * 32, o);
+          tmem_ld_wait();
+        }
         if (valid && has) {
           float* dst = reinterpret_cast<float*>(p.out) + row_off + c * 32;
 #pragma unroll
@@ -321,7 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c = 0; c < D / 32; ++c) {
         uint32_t o[32];
         if (n_total > 0) {
-          tmem_ld32(tmem_o + lane_off + c * 32, o);
+          tmem_ld32(t_o + c * 32, o);
           tmem_ld_wait();
         }
         if (!valid) continue;
@@ -355,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -378,6 +415,7 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
 
 }  // namespace
 
+// tiles/items: the plan's 256-row q-major work list (FfaPlan::fwd2_*).
 cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_tiles,
                            int seqlen_q, int seqlen_k, int hq, int hk, int head_dim,
                            float softmax_scale, const void* q, const void* k, const void* v,
