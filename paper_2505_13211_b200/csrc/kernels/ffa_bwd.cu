@@ -4,15 +4,27 @@
 // kernels so every gradient element has exactly one producing CTA and one
 // fixed accumulation order:
 //
-//   dkdv kernel (k-major): one CTA per (128-key tile, key/value head). It walks
-//     every (q-head of the GQA group, slice item, q-tile) touching its keys:
-//       S^T  = K Q^T            (TMEM)       dP^T = V dO^T      (TMEM)
-//       P^T  = exp2(S^T*c - lse) (regs -> TMEM as packed bf16, aliasing S^T)
-//       dS^T = P^T (dP^T - delta)  (regs -> smem, bf16)
-//       dV  += P^T dO  (tcgen05.mma A-from-TMEM)   dK += dS^T Q  (SS)
-//     dK/dV stay in TMEM for the whole walk and are written once.
-//   dq kernel (q-major): one CTA per (128-query tile, q-head), the forward's
-//     work list: S = Q K^T, dP = dO V^T, dS = P (dP - delta), dQ += dS K.
+//   dkdv kernel (k-major): one CTA per (128-key tile, key/value head), walking
+//     every (q head of the GQA group, slice item, 128-query tile) that touches
+//     its keys:
+//       S^T  = K Q^T,  dP^T = V dO^T                     (TMEM)
+//       P^T  = exp2(S^T c - lse)   kept in registers, then packed bf16 into
+//                                  the consumed dP^T columns (TMEM)
+//       dS^T = P^T (dP^T - delta) -> smem (bf16)
+//       dV  += P^T dO  (A from TMEM)   dK += dS^T Q  (A from smem)
+//     dK / dV accumulate in TMEM over the whole walk and are written once.
+//   dq kernel (q-major): one CTA per (128-query tile, q head) over the
+//     forward work list: S = Q K^T, dP = dO V^T, dS = P (dP - delta) -> smem,
+//     dQ += dS K (TMEM).
+//
+// Overlap comes from issue order, not extra accumulators (TMEM is full): the
+// elementwise warps signal "S consumed" as soon as S(t) sits in registers, so
+// the MMA warp issues S(t+1) while they exponentiate; the gradient MMAs of
+// step t follow, then dP(t+1) into the dP region they just released. Every
+// other hand-off is implied by in-order MMA completion (dP(t+1) done => the
+// gradient MMAs of step t, which read the dS smem tile and the P columns,
+// retired). All MMAs are M=128, N=128 (or N=D), K=16: at that shape the SS
+// operand traffic stays within the shared-memory port.
 //
 // Warp roles in both: warps 0-3 elementwise (thread = TMEM lane = one row),
 // warp 4 TMA producer, warp 5 MMA issuer.
@@ -27,9 +39,10 @@
 namespace magi {
 namespace {
 
-constexpr uint32_t kBox = 128 * 64 * 2;
+constexpr uint32_t kBox = 128 * 64 * 2;  // 128 rows x 64 bf16, 128B swizzle
 constexpr int kThreads = 192;
 constexpr int kMath = 128;
+constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
 struct BwdParams {
@@ -49,7 +62,6 @@ struct BwdParams {
   int32_t accumulate;
 };
 
-template <int D>
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
                                           int c, float scale, bool f32, bool accumulate) {
   if (f32) {
@@ -84,24 +96,73 @@ __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint
   }
 }
 
+// Write a D-wide TMEM accumulator row to global memory (zeros when the CTA
+// had no work; nothing when accumulating nothing).
+template <int D>
+__device__ __forceinline__ void epilogue_rows(uint32_t t_acc, bool has_work, bool valid, void* base,
+                                              size_t row_off, float scale, bool f32, bool acc) {
+#pragma unroll 1
+  for (int c = 0; c < D / 32; ++c) {
+    uint32_t o[32];
+    if (has_work) {
+      tmem_ld32(t_acc + c * 32, o);
+      tmem_ld_wait();
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = 0u;
+    }
+    if (valid && !(acc && !has_work)) store_row(base, row_off, o, c, scale, f32, acc);
+  }
+}
+
+// D[tmem] (M=128, N=128) = A[128 rows, D] . B[128 rows, D]^T, both K-major.
+template <int D>
+__device__ __forceinline__ void mma_rows_x_rows(uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr) {
+  constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+#pragma unroll
+  for (int k = 0; k < D / 16; ++k) {
+    const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+    umma_bf16_ss(d_tmem, make_smem_desc(a_addr + off, 16, 1024), make_smem_desc(b_addr + off, 16, 1024),
+                 idesc, k > 0);
+  }
+}
+
+// 64 packed bf16-pair registers holding 128 values -> 16 x 16B swizzled smem chunks of one row.
+__device__ __forceinline__ void store_row_sw128(uint8_t* tile, int row, const uint32_t* v) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    *reinterpret_cast<uint4*>(tile + (c / 8) * kBox + sw128_offset(row, c % 8)) =
+        make_uint4(v[c * 4 + 0], v[c * 4 + 1], v[c * 4 + 2], v[c * 4 + 3]);
+  }
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
 // =========================================================================== dK / dV
 template <int D>
 struct DkvSmem {
   static constexpr uint32_t kTile = (D / 64) * kBox;
   static constexpr uint32_t kK = 0;
   static constexpr uint32_t kV = kK + kTile;
-  static constexpr uint32_t kQ = kV + kTile;           // 2 stages
-  static constexpr uint32_t kDO = kQ + 2 * kTile;      // 2 stages
-  static constexpr uint32_t kDS = kDO + 2 * kTile;     // dS^T [keys, q] bf16, 2 boxes
-  static constexpr uint32_t kLse = kDS + 2 * kBox;      // [128] f32 (log2 domain)
+  static constexpr uint32_t kQ = kV + kTile;               // kStages
+  static constexpr uint32_t kDO = kQ + kStages * kTile;    // kStages
+  static constexpr uint32_t kDS = kDO + kStages * kTile;   // dS^T [128 keys, 128 q] bf16
+  static constexpr uint32_t kLse = kDS + 2 * kBox;         // [128] f32 (log2 domain)
   static constexpr uint32_t kDelta = kLse + kBlockM * 4;
   static constexpr uint32_t kBytes = kDelta + kBlockM * 4;
 };
 
 struct DkvBarriers {
   uint64_t kv_full;
-  uint64_t qdo_full[2], qdo_empty[2];
-  uint64_t s_full, p_full, mma_done;
+  uint64_t qdo_full[kStages], qdo_empty[kStages];
+  uint64_t s_full, s_free, dp_full, p_full, done;
 };
 
 template <int D>
@@ -126,13 +187,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars.qdo_full[s], 1);
       mbar_init(&bars.qdo_empty[s], 1);
     }
     mbar_init(&bars.s_full, 1);
+    mbar_init(&bars.s_free, kMath);
+    mbar_init(&bars.dp_full, 1);
     mbar_init(&bars.p_full, kMath);
-    mbar_init(&bars.mma_done, 1);
+    mbar_init(&bars.done, 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(&tmem_slot);
@@ -140,9 +203,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
-  const uint32_t t_st = tmem;          // S^T, then packed P^T in its first 64 columns
-  const uint32_t t_dpt = tmem + 128;   // dP^T
-  const uint32_t t_dv = tmem + 256;    // dV  [keys, D]
+  const uint32_t t_st = tmem;            // S^T
+  const uint32_t t_dpt = tmem + 128;     // dP^T, then P^T packed in its first 64 columns
+  const uint32_t t_dv = tmem + 256;      // dV [keys, D]
   const uint32_t t_dk = tmem + 256 + D;  // dK [keys, D]
 
   uint8_t* sK = smem + L::kK;
@@ -177,60 +240,69 @@ __global__ void __launch_bounds__(kThreads, 1)
               tma_load_3d(sDO + st.index * L::kTile + c * kBox, &tmap_do,
                           &bars.qdo_full[st.index], c * 64, h, q0);
             }
-            st.advance<2>();
+            st.advance<kStages>();
           }
         }
       }
     }
   } else if (warp == 5) {
     if (lane == 0 && steps > 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_g = make_idesc_bf16(128, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sDS);
       mbar_wait(&bars.kv_full, 0);
-      PipeState st;
+      PipeState nst;  // stage of the next S / dP issue
+      PipeState gst;  // stage of the gradient MMAs
+      mbar_wait(&bars.qdo_full[nst.index], nst.phase);
+      tc_fence_after();
+      mma_rows_x_rows<D>(t_st, k_addr, smem_u32(sQ + nst.index * L::kTile));
+      umma_commit(&bars.s_full);
+      mma_rows_x_rows<D>(t_dpt, v_addr, smem_u32(sDO + nst.index * L::kTile));
+      umma_commit(&bars.dp_full);
+      nst.advance<kStages>();
       for (int t = 0; t < steps; ++t) {
-        mbar_wait(&bars.qdo_full[st.index], st.phase);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQ + st.index * L::kTile);
-        const uint32_t do_addr = smem_u32(sDO + st.index * L::kTile);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-          umma_bf16_ss(t_st, make_smem_desc(k_addr + off, 16, 1024),
-                       make_smem_desc(q_addr + off, 16, 1024), idesc_s, k > 0);
+        const bool more = t + 1 < steps;
+        if (more) {
+          // S(t+1) as soon as S(t) is in registers
+          mbar_wait(&bars.s_free, t & 1);
+          mbar_wait(&bars.qdo_full[nst.index], nst.phase);
+          tc_fence_after();
+          mma_rows_x_rows<D>(t_st, k_addr, smem_u32(sQ + nst.index * L::kTile));
+          umma_commit(&bars.s_full);
         }
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-          umma_bf16_ss(t_dpt, make_smem_desc(v_addr + off, 16, 1024),
-                       make_smem_desc(do_addr + off, 16, 1024), idesc_s, k > 0);
-        }
-        umma_commit(&bars.s_full);
         mbar_wait(&bars.p_full, t & 1);
         tc_fence_after();
+        const uint32_t q_addr = smem_u32(sQ + gst.index * L::kTile);
+        const uint32_t do_addr = smem_u32(sDO + gst.index * L::kTile);
 #pragma unroll
         for (int k = 0; k < kBlockM / 16; ++k) {
-          // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] (MN-major)
-          umma_bf16_ts(t_dv, t_st + k * 8, make_smem_desc(do_addr + k * 16 * 128, kBox, 1024),
-                       idesc_g, (t > 0 || k > 0) ? 1u : 0u);
+          // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] MN-major
+          umma_bf16_ts(t_dv, t_dpt + k * 8, make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
+                       (t > 0 || k > 0) ? 1u : 0u);
         }
 #pragma unroll
         for (int k = 0; k < kBlockM / 16; ++k) {
-          // dK += dS^T Q : A = dS^T [keys, q] (K-major smem), B = Q [q, D] (MN-major)
+          // dK += dS^T Q : A = dS^T [keys, q] K-major smem, B = Q [q, D] MN-major
           umma_bf16_ss(t_dk, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
                        make_smem_desc(q_addr + k * 16 * 128, kBox, 1024), idesc_g,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&bars.mma_done);
-        umma_commit(&bars.qdo_empty[st.index]);
-        st.advance<2>();
+        umma_commit(&bars.qdo_empty[gst.index]);
+        gst.advance<kStages>();
+        if (more) {
+          // dP(t+1) into the columns the gradient MMAs above read (in-order pipe)
+          mma_rows_x_rows<D>(t_dpt, v_addr, smem_u32(sDO + nst.index * L::kTile));
+          umma_commit(&bars.dp_full);
+          nst.advance<kStages>();
+        } else {
+          umma_commit(&bars.done);
+        }
       }
     }
   } else {
     const int row = warp * 32 + lane;
     const int key = tile.k0 + row;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const float sl2 = p.scale_log2;
     int t = 0;
     for (int g = 0; g < group; ++g) {
       const int h = head_k * group + g;
@@ -248,8 +320,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < item.n_qtiles; ++i, ++t) {
           const int q0 = item.q_begin + i * kBlockM;
-          // every math thread is done reading the previous step's lse/delta
-          named_bar_sync(1, kMath);
+          float* lse_b = s_lse;
+          float* delta_b = s_delta;
+          named_bar_sync(1, kMath);  // every math thread is done with the previous step's values
           {
             const int qq = q0 + row;
             float l = INFINITY, dlt = 0.f;
@@ -258,54 +331,54 @@ __global__ void __launch_bounds__(kThreads, 1)
               l = raw == -INFINITY ? INFINITY : raw * kLog2e;
               dlt = delta_h[qq];
             }
-            s_lse[row] = l;
-            s_delta[row] = dlt;
+            lse_b[row] = l;
+            delta_b[row] = dlt;
           }
           named_bar_sync(1, kMath);
           mbar_wait(&bars.s_full, t & 1);
-          // keeps this thread at most one mma_done phase behind, so the final
-          // parity wait below cannot alias an older phase
-          if (t > 0) mbar_wait(&bars.mma_done, (t - 1) & 1);
           tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < kBlockM / 32; ++c) {
-            uint32_t s[32], dp[32];
-            tmem_ld32(t_st + lane_off + c * 32, s);
+          float pv[128];
+          {
+            uint32_t s[128];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
+              tmem_ld32(t_st + lane_off + c * 32, chunk);
+            }
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&bars.s_free);
+            const bool all_in = qlo <= q0 && q0 + kBlockM <= qhi;
+#pragma unroll
+            for (int c = 0; c < 128; ++c) {
+              const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_b[c]);
+              const float e = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+              pv[c] = (all_in || (q0 + c >= qlo && q0 + c < qhi)) ? e : 0.f;
+            }
+          }
+          mbar_wait(&bars.dp_full, t & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t dp[32];
             tmem_ld32(t_dpt + lane_off + c * 32, dp);
             tmem_ld_wait();
-            uint32_t pk[16], dk[16];
+            uint32_t pk[16], ds[16];
 #pragma unroll
             for (int j = 0; j < 32; j += 2) {
-              float pv[2], dv[2];
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int col = c * 32 + j + u;
-                const int qq = q0 + col;
-                const bool ok = qq >= qlo && qq < qhi;
-                const float e = fast_exp2(__uint_as_float(s[j + u]) * p.scale_log2 - s_lse[col]);
-                pv[u] = ok ? e : 0.f;
-                dv[u] = pv[u] * (__uint_as_float(dp[j + u]) - s_delta[col]);
-              }
-              pk[j / 2] = pack_bf16(pv[0], pv[1]);
-              dk[j / 2] = pack_bf16(dv[0], dv[1]);
+              const int col = c * 32 + j;
+              pk[j / 2] = pack_bf16(pv[col], pv[col + 1]);
+              ds[j / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - delta_b[col]),
+                                    pv[col + 1] * (__uint_as_float(dp[j + 1]) - delta_b[col + 1]));
             }
-            // P^T chunk -> TMEM columns [c*16, c*16+16) (already-consumed S^T columns)
-            uint32_t pk32[32];
-#pragma unroll
-            for (int j = 0; j < 16; ++j) pk32[j] = pk[j];
-            asm volatile(
-                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
-                "%12,%13,%14,%15,%16};" ::"r"(t_st + lane_off + c * 16),
-                "r"(pk32[0]), "r"(pk32[1]), "r"(pk32[2]), "r"(pk32[3]), "r"(pk32[4]), "r"(pk32[5]),
-                "r"(pk32[6]), "r"(pk32[7]), "r"(pk32[8]), "r"(pk32[9]), "r"(pk32[10]),
-                "r"(pk32[11]), "r"(pk32[12]), "r"(pk32[13]), "r"(pk32[14]), "r"(pk32[15])
-                : "memory");
+            // P^T chunk -> dP^T columns [c*16, c*16+16) (already consumed)
+            tmem_st16(t_dpt + lane_off + c * 16, pk);
             // dS^T chunk -> smem row `row`, q columns [c*32, c*32+32)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int chunk16 = c * 4 + u;  // 16-byte chunk index over 128 q columns
-              uint4 v = make_uint4(dk[u * 4 + 0], dk[u * 4 + 1], dk[u * 4 + 2], dk[u * 4 + 3]);
-              *reinterpret_cast<uint4*>(sDS + (chunk16 / 8) * kBox + sw128_offset(row, chunk16 % 8)) = v;
+              const int ch = c * 4 + u;
+              *reinterpret_cast<uint4*>(sDS + (ch / 8) * kBox + sw128_offset(row, ch % 8)) =
+                  make_uint4(ds[u * 4 + 0], ds[u * 4 + 1], ds[u * 4 + 2], ds[u * 4 + 3]);
             }
           }
           tmem_st_wait();
@@ -315,38 +388,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    // epilogue: dV, dK rows
     if (steps > 0) {
-      mbar_wait(&bars.mma_done, (steps - 1) & 1);
+      mbar_wait(&bars.done, 0);
       tc_fence_after();
     }
     const bool valid = key < p.seqlen_k;
     const size_t row_off = (static_cast<size_t>(key) * p.hk + head_k) * D;
     const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      if (steps > 0) {
-        tmem_ld32(t_dv + lane_off + c * 32, o);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0u;
-      }
-      if (valid && !(acc && steps == 0)) store_row<D>(p.dv, row_off, o, c, 1.f, f32, acc);
-    }
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      if (steps > 0) {
-        tmem_ld32(t_dk + lane_off + c * 32, o);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0u;
-      }
-      if (valid && !(acc && steps == 0)) store_row<D>(p.dk, row_off, o, c, p.scale, f32, acc);
-    }
+    epilogue_rows<D>(t_dv + lane_off, steps > 0, valid, p.dv, row_off, 1.f, f32, acc);
+    epilogue_rows<D>(t_dk + lane_off, steps > 0, valid, p.dk, row_off, p.scale, f32, acc);
   }
 
   tc_fence_before();
@@ -363,16 +413,16 @@ struct DqSmem {
   static constexpr uint32_t kTile = (D / 64) * kBox;
   static constexpr uint32_t kQ = 0;
   static constexpr uint32_t kDO = kQ + kTile;
-  static constexpr uint32_t kK = kDO + kTile;       // 2 stages
-  static constexpr uint32_t kV = kK + 2 * kTile;    // 2 stages
-  static constexpr uint32_t kDS = kV + 2 * kTile;   // dS [q, keys] bf16, 2 boxes
+  static constexpr uint32_t kK = kDO + kTile;             // kStages
+  static constexpr uint32_t kV = kK + kStages * kTile;    // kStages
+  static constexpr uint32_t kDS = kV + kStages * kTile;   // dS [q, keys] bf16
   static constexpr uint32_t kBytes = kDS + 2 * kBox;
 };
 
 struct DqBarriers {
   uint64_t qdo_full;
-  uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-  uint64_t s_full, s_free, ds_full, dq_done;
+  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  uint64_t s_full, s_free, dp_full, p_full, done;
 };
 
 template <int D>
@@ -397,7 +447,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.qdo_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&bars.k_full[s], 1);
       mbar_init(&bars.k_empty[s], 1);
       mbar_init(&bars.v_full[s], 1);
@@ -405,8 +455,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_init(&bars.s_full, 1);
     mbar_init(&bars.s_free, kMath);
-    mbar_init(&bars.ds_full, kMath);
-    mbar_init(&bars.dq_done, 1);
+    mbar_init(&bars.dp_full, 1);
+    mbar_init(&bars.p_full, kMath);
+    mbar_init(&bars.done, 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(&tmem_slot);
@@ -446,49 +497,38 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < D / 64; ++c)
             tma_load_3d(sV + st.index * L::kTile + c * kBox, &tmap_v, &bars.v_full[st.index],
                         c * 64, head_k, k0);
-          st.advance<2>();
+          st.advance<kStages>();
         }
       }
     }
   } else if (warp == 5) {
     if (lane == 0 && steps > 0) {
-      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, false, true);
       const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
       mbar_wait(&bars.qdo_full, 0);
-      PipeState kst, vst;
-      auto issue_s = [&](int t) {
-        if (t > 0) mbar_wait(&bars.s_free, (t - 1) & 1);
-        mbar_wait(&bars.k_full[kst.index], kst.phase);
-        mbar_wait(&bars.v_full[vst.index], vst.phase);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + kst.index * L::kTile);
-        const uint32_t v_addr = smem_u32(sV + vst.index * L::kTile);
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-          umma_bf16_ss(t_s, make_smem_desc(q_addr + off, 16, 1024),
-                       make_smem_desc(k_addr + off, 16, 1024), idesc_s, k > 0);
-        }
-#pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-          umma_bf16_ss(t_dp, make_smem_desc(do_addr + off, 16, 1024),
-                       make_smem_desc(v_addr + off, 16, 1024), idesc_s, k > 0);
-        }
-        umma_commit(&bars.s_full);
-        umma_commit(&bars.v_empty[vst.index]);
-        vst.advance<2>();
-      };
-      issue_s(0);
-      PipeState kuse;  // stage of the K tile dQ_t consumes
+      PipeState nst, gst;
+      mbar_wait(&bars.k_full[nst.index], nst.phase);
+      mbar_wait(&bars.v_full[nst.index], nst.phase);
+      tc_fence_after();
+      mma_rows_x_rows<D>(t_s, q_addr, smem_u32(sK + nst.index * L::kTile));
+      umma_commit(&bars.s_full);
+      mma_rows_x_rows<D>(t_dp, do_addr, smem_u32(sV + nst.index * L::kTile));
+      umma_commit(&bars.dp_full);
+      umma_commit(&bars.v_empty[nst.index]);
+      nst.advance<kStages>();
       for (int t = 0; t < steps; ++t) {
-        const PipeState kcur = kuse;
-        kst.advance<2>();
-        if (t + 1 < steps) issue_s(t + 1);
-        mbar_wait(&bars.ds_full, t & 1);
+        const bool more = t + 1 < steps;
+        if (more) {
+          mbar_wait(&bars.s_free, t & 1);
+          mbar_wait(&bars.k_full[nst.index], nst.phase);
+          mbar_wait(&bars.v_full[nst.index], nst.phase);
+          tc_fence_after();
+          mma_rows_x_rows<D>(t_s, q_addr, smem_u32(sK + nst.index * L::kTile));
+          umma_commit(&bars.s_full);
+        }
+        mbar_wait(&bars.p_full, t & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + kcur.index * L::kTile);
+        const uint32_t k_addr = smem_u32(sK + gst.index * L::kTile);
 #pragma unroll
         for (int k = 0; k < kBlockN / 16; ++k) {
           // dQ += dS K : A = dS [q, keys] K-major, B = K [keys, D] MN-major
@@ -496,9 +536,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                        make_smem_desc(k_addr + k * 16 * 128, kBox, 1024), idesc_q,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(&bars.dq_done);
-        umma_commit(&bars.k_empty[kcur.index]);
-        kuse.advance<2>();
+        umma_commit(&bars.k_empty[gst.index]);
+        gst.advance<kStages>();
+        if (more) {
+          mma_rows_x_rows<D>(t_dp, do_addr, smem_u32(sV + nst.index * L::kTile));
+          umma_commit(&bars.dp_full);
+          umma_commit(&bars.v_empty[nst.index]);
+          nst.advance<kStages>();
+        } else {
+          umma_commit(&bars.done);
+        }
       }
     }
   } else {
@@ -506,6 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int q = tile.q0 + row;
     const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
     const bool valid = q < p.seqlen_q;
+    const float sl2 = p.scale_log2;
     float lse_l2 = INFINITY, dlt = 0.f;
     if (valid) {
       const float raw = p.lse[static_cast<size_t>(head) * p.seqlen_q + q];
@@ -521,57 +569,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = item.k_begin + j * kBlockN;
         mbar_wait(&bars.s_full, t & 1);
         tc_fence_after();
+        float pv[128];
+        {
+          uint32_t s[128];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
+            tmem_ld32(t_s + lane_off + c * 32, chunk);
+          }
+          tmem_ld_wait();
+          tc_fence_before();
+          mbar_arrive(&bars.s_free);
+          const bool all_in = lo <= k0 && k0 + kBlockN <= hi;
+#pragma unroll
+          for (int c = 0; c < 128; ++c) {
+            const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
+            const float e = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+            pv[c] = (all_in || (k0 + c >= lo && k0 + c < hi)) ? e : 0.f;
+          }
+        }
+        mbar_wait(&bars.dp_full, t & 1);
+        tc_fence_after();
         uint32_t ds[64];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          uint32_t s[32], dp[32];
-          tmem_ld32(t_s + lane_off + c * 32, s);
+          uint32_t dp[32];
           tmem_ld32(t_dp + lane_off + c * 32, dp);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2) {
-            float v2[2];
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-              const int col = k0 + c * 32 + i + u;
-              const bool ok = col >= lo && col < hi;
-              const float e = fast_exp2(__uint_as_float(s[i + u]) * p.scale_log2 - lse_l2);
-              v2[u] = ok ? e * (__uint_as_float(dp[i + u]) - dlt) : 0.f;
-            }
-            ds[c * 16 + i / 2] = pack_bf16(v2[0], v2[1]);
+          for (int j = 0; j < 32; j += 2) {
+            const int col = c * 32 + j;
+            ds[col / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - dlt),
+                                    pv[col + 1] * (__uint_as_float(dp[j + 1]) - dlt));
           }
         }
-        tc_fence_before();
-        mbar_arrive(&bars.s_free);
-        if (t > 0) mbar_wait(&bars.dq_done, (t - 1) & 1);
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-          *reinterpret_cast<uint4*>(sDS + (c / 8) * kBox + sw128_offset(row, c % 8)) =
-              make_uint4(ds[c * 4 + 0], ds[c * 4 + 1], ds[c * 4 + 2], ds[c * 4 + 3]);
-        }
+        store_row_sw128(sDS, row, ds);
         fence_proxy_async_smem();
         tc_fence_before();
-        mbar_arrive(&bars.ds_full);
+        mbar_arrive(&bars.p_full);
       }
     }
     if (steps > 0) {
-      mbar_wait(&bars.dq_done, (steps - 1) & 1);
+      mbar_wait(&bars.done, 0);
       tc_fence_after();
     }
     const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D;
-    const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
-#pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t o[32];
-      if (steps > 0) {
-        tmem_ld32(t_dq + lane_off + c * 32, o);
-        tmem_ld_wait();
-      } else {
-#pragma unroll
-        for (int i = 0; i < 32; ++i) o[i] = 0u;
-      }
-      if (valid && !(acc && steps == 0)) store_row<D>(p.dq, row_off, o, c, p.scale, f32, acc);
-    }
+    epilogue_rows<D>(t_dq + lane_off, steps > 0, valid, p.dq, row_off, p.scale, p.grad_f32 != 0,
+                     p.accumulate != 0);
   }
 
   tc_fence_before();
@@ -610,7 +654,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
                                                                                  prm);
     err = cudaGetLastError();
   }
-  return err == cudaSuccess ? cudaGetLastError() : err;
+  return err;
 }
 
 }  // namespace
