@@ -78,7 +78,6 @@ magiplan_ffa_plan* make_plan(std::vector<magi::SliceGeom> slices, int64_t sq, in
     handle->plan.head_dim = head_dim;
     handle->plan.slices = std::move(slices);
     magiplan::build_ffa_worklists(handle->plan);
-    magiplan::upload_ffa_worklists(handle->plan);
   } catch (...) {
     delete handle;
     throw;
@@ -143,7 +142,8 @@ magiplan_status magiplan_ffa_fwd(const magiplan_ffa_plan* plan, const void* q, c
   return guarded([&] {
     check_heads(num_heads_q, num_heads_k);
     check_dtype(out_dtype, accumulate);
-    const auto& P = plan->plan;
+    auto& P = const_cast<magiplan_ffa_plan*>(plan)->plan;
+    magiplan::ensure_uploaded(P);
     cuda_check(magi::launch_ffa_fwd(P.d_fwd2_tiles, P.d_fwd2_items,
                                     static_cast<int>(P.fwd2_tiles.size()),
                                     static_cast<int>(P.seqlen_q), static_cast<int>(P.seqlen_k),
@@ -179,7 +179,8 @@ magiplan_status ffa_bwd_parts(const magiplan_ffa_plan* plan, const void* q, cons
   return guarded([&] {
     check_heads(num_heads_q, num_heads_k);
     check_dtype(grad_dtype, accumulate);
-    const auto& P = plan->plan;
+    auto& P = const_cast<magiplan_ffa_plan*>(plan)->plan;
+    magiplan::ensure_uploaded(P);
     cuda_check(
         magi::launch_ffa_bwd(P.d_fwd_tiles, P.d_fwd_items, static_cast<int>(P.fwd_tiles.size()),
                              P.d_bwd_tiles, P.d_bwd_items, static_cast<int>(P.bwd_tiles.size()),

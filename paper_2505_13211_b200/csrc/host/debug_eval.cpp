@@ -4,6 +4,7 @@
 #include <nlohmann/json.hpp>
 
 #include "errors.hpp"
+#include "ffa_plan.hpp"
 #include "scenario.hpp"
 
 namespace magiplan {
@@ -116,6 +117,41 @@ std::string debug_eval(const std::string& request) {
     out = lognormal_lengths(r["count"].get<std::size_t>(), r["median"].get<double>(),
                             r["sigma"].get<double>(), r["max_length"].get<Token>(),
                             r["seed"].get<uint64_t>());
+  } else if (op == "ffa_worklists") {
+    // host-side FFA work lists of a slice list (no device involved)
+    FfaPlan plan;
+    plan.seqlen_q = r["seqlen_q"].get<int64_t>();
+    plan.seqlen_k = r["seqlen_k"].get<int64_t>();
+    plan.head_dim = r.value("head_dim", 128);
+    for (const auto& s : r["slices"]) {
+      plan.slices.push_back({s[0].get<int32_t>(), s[1].get<int32_t>(), s[2].get<int32_t>(),
+                             s[3].get<int32_t>(), s[4].get<int32_t>()});
+    }
+    build_ffa_worklists(plan);
+    auto qmajor = [](const std::vector<magi::FwdTile>& tiles, const std::vector<magi::FwdItem>& items) {
+      json out = json::array();
+      for (const auto& t : tiles) {
+        json jt = {{"q0", t.q0}, {"n_ktiles", t.n_ktiles}, {"items", json::array()}};
+        for (int i = t.item_begin; i < t.item_end; ++i) {
+          const auto& it = items[static_cast<std::size_t>(i)];
+          jt["items"].push_back({it.qs, it.qe, it.ks, it.ke, it.type, it.k_begin, it.n_ktiles});
+        }
+        out.push_back(jt);
+      }
+      return out;
+    };
+    out["fwd128"] = qmajor(plan.fwd_tiles, plan.fwd_items);
+    out["fwd256"] = qmajor(plan.fwd2_tiles, plan.fwd2_items);
+    out["bwd"] = json::array();
+    for (const auto& t : plan.bwd_tiles) {
+      json jt = {{"k0", t.k0}, {"n_qtiles", t.n_qtiles}, {"items", json::array()}};
+      for (int i = t.item_begin; i < t.item_end; ++i) {
+        const auto& it = plan.bwd_items[static_cast<std::size_t>(i)];
+        jt["items"].push_back({it.qs, it.qe, it.ks, it.ke, it.type, it.q_begin, it.n_qtiles});
+      }
+      out["bwd"].push_back(jt);
+    }
+    out["area_multiplicity"] = plan.area_multiplicity;
   } else if (op == "flops") {
     WorkloadSpec w;
     w.num_heads_q = r["num_heads_q"].get<int64_t>();

@@ -256,13 +256,24 @@ void build_kmajor(FfaPlan& plan) {
 
 }  // namespace
 
-void upload_ffa_worklists(FfaPlan& plan) {
+void ensure_uploaded(FfaPlan& plan) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) throw DeviceError("ffa plan: no CUDA device");
+  std::lock_guard<std::mutex> lock(plan.upload_mutex);
+  if (plan.device >= 0) {
+    if (plan.device != dev) {
+      throw UsageError("ffa plan lives on device " + std::to_string(plan.device) +
+                       " but was used on device " + std::to_string(dev));
+    }
+    return;
+  }
   plan.d_fwd_tiles = upload(plan.fwd_tiles);
   plan.d_fwd_items = upload(plan.fwd_items);
   plan.d_fwd2_tiles = upload(plan.fwd2_tiles);
   plan.d_fwd2_items = upload(plan.fwd2_items);
   plan.d_bwd_tiles = upload(plan.bwd_tiles);
   plan.d_bwd_items = upload(plan.bwd_items);
+  plan.device = dev;
 }
 
 }  // namespace magiplan

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -31,6 +32,8 @@ struct FfaPlan {
   magi::FwdItem* d_fwd2_items = nullptr;
   magi::BwdTile* d_bwd_tiles = nullptr;
   magi::BwdItem* d_bwd_items = nullptr;
+  int device = -1;  // device holding the copies (-1: not uploaded yet)
+  std::mutex upload_mutex;
 
   FfaPlan() = default;
   FfaPlan(const FfaPlan&) = delete;
@@ -46,7 +49,9 @@ struct FfaPlan {
 // AttnMask::check_valid, reference proj/src/mask.cpp:175-191) and builds the
 // host work lists; does not touch the device.
 void build_ffa_worklists(FfaPlan& plan);
-// Uploads the work lists (synchronous cudaMemcpy); DeviceError on failure.
-void upload_ffa_worklists(FfaPlan& plan);
+// Uploads the work lists to the current device on first use (thread-safe,
+// synchronous cudaMemcpy). DeviceError on CUDA failure; UsageError when the
+// plan is later used from a different device than the one it lives on.
+void ensure_uploaded(FfaPlan& plan);
 
 }  // namespace magiplan

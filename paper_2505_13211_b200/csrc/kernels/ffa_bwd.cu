@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "ffa_common.cuh"
 #include "sm100.cuh"
@@ -40,8 +41,10 @@ namespace magi {
 namespace {
 
 constexpr uint32_t kBox = 128 * 64 * 2;  // 128 rows x 64 bf16, 128B swizzle
-constexpr int kThreads = 192;
-constexpr int kMath = 128;
+constexpr int kThreads = 320;  // 8 elementwise warps + TMA warp + MMA warp
+constexpr int kTmaWarp = 8;
+constexpr int kMmaWarp = 9;
+constexpr int kMath = 256;
 constexpr int kStages = 2;
 constexpr float kLog2e = 1.4426950408889634f;
 
@@ -60,6 +63,7 @@ struct BwdParams {
   void* dv;
   int32_t grad_f32;
   int32_t accumulate;
+  int32_t experiment;  // diagnostics: 1 = no elementwise work, 2 = no gradient MMAs
 };
 
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
@@ -154,16 +158,22 @@ struct DkvSmem {
   static constexpr uint32_t kQ = kV + kTile;               // kStages
   static constexpr uint32_t kDO = kQ + kStages * kTile;    // kStages
   static constexpr uint32_t kDS = kDO + kStages * kTile;   // dS^T [128 keys, 128 q] bf16
-  static constexpr uint32_t kLse = kDS + 2 * kBox;         // [128] f32 (log2 domain)
-  static constexpr uint32_t kDelta = kLse + kBlockM * 4;
-  static constexpr uint32_t kBytes = kDelta + kBlockM * 4;
+  static constexpr uint32_t kLse = kDS + 2 * kBox;         // kStages x [128] f32 (log2 domain)
+  static constexpr uint32_t kDelta = kLse + kStages * kBlockM * 4;
+  static constexpr uint32_t kBars = kDelta + kStages * kBlockM * 4;
+  static constexpr uint32_t kBytes = kBars + 128;          // barriers + TMEM slot
 };
 
+// Lives in dynamic shared memory right after the tiles: with no static
+// shared memory the 1024-aligned dynamic window starts at offset 0, which is
+// what lets 227 KB of tiles fit without an alignment slack.
 struct DkvBarriers {
   uint64_t kv_full;
   uint64_t qdo_full[kStages], qdo_empty[kStages];
   uint64_t s_full, s_free, dp_full, p_full, done;
+  uint32_t tmem_slot;
 };
+static_assert(sizeof(DkvBarriers) <= 128, "barrier block");
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -172,11 +182,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const __grid_constant__ CUtensorMap tmap_v,
                         const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
   using L = DkvSmem<D>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
-  __shared__ DkvBarriers bars;
-  __shared__ uint32_t tmem_slot;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  DkvBarriers& bars = *reinterpret_cast<DkvBarriers*>(smem + L::kBars);
+  uint32_t& tmem_slot = bars.tmem_slot;
+  if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-byte alignment
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tile_rank = blockIdx.x / p.hk;
@@ -188,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bars.qdo_full[s], 1);
+      // TMA bytes (lane 0's expect_tx arrival) + one arrival per producer lane
+      // after it stored the stage's lse / delta
+      mbar_init(&bars.qdo_full[s], 1 + 32);
       mbar_init(&bars.qdo_empty[s], 1);
     }
     mbar_init(&bars.s_full, 1);
@@ -198,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars.done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<512>(&tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(&tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -216,36 +227,59 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* s_lse = reinterpret_cast<float*>(smem + L::kLse);
   float* s_delta = reinterpret_cast<float*>(smem + L::kDelta);
 
-  if (warp == 4) {
-    if (lane == 0 && steps > 0) {
-      tma_prefetch_desc(&tmap_q);
-      tma_prefetch_desc(&tmap_do);
-      mbar_arrive_expect_tx(&bars.kv_full, 2 * L::kTile);
-      for (int c = 0; c < D / 64; ++c) {
-        tma_load_3d(sK + c * kBox, &tmap_k, &bars.kv_full, c * 64, head_k, tile.k0);
-        tma_load_3d(sV + c * kBox, &tmap_v, &bars.kv_full, c * 64, head_k, tile.k0);
+  if (warp == kTmaWarp) {
+    if (steps > 0) {
+      if (lane == 0) {
+        tma_prefetch_desc(&tmap_q);
+        tma_prefetch_desc(&tmap_do);
+        mbar_arrive_expect_tx(&bars.kv_full, 2 * L::kTile);
+        for (int c = 0; c < D / 64; ++c) {
+          tma_load_3d(sK + c * kBox, &tmap_k, &bars.kv_full, c * 64, head_k, tile.k0);
+          tma_load_3d(sV + c * kBox, &tmap_v, &bars.kv_full, c * 64, head_k, tile.k0);
+        }
       }
       PipeState st;
       for (int g = 0; g < group; ++g) {
         const int h = head_k * group + g;
+        const float* lse_h = p.lse + static_cast<size_t>(h) * p.seqlen_q;
+        const float* delta_h = p.delta + static_cast<size_t>(h) * p.seqlen_q;
         for (int it = tile.item_begin; it < tile.item_end; ++it) {
           const BwdItem item = p.k_items[it];
           for (int i = 0; i < item.n_qtiles; ++i) {
             const int q0 = item.q_begin + i * kBlockM;
             mbar_wait(&bars.qdo_empty[st.index], st.phase ^ 1);
-            mbar_arrive_expect_tx(&bars.qdo_full[st.index], 2 * L::kTile);
-            for (int c = 0; c < D / 64; ++c) {
-              tma_load_3d(sQ + st.index * L::kTile + c * kBox, &tmap_q, &bars.qdo_full[st.index],
-                          c * 64, h, q0);
-              tma_load_3d(sDO + st.index * L::kTile + c * kBox, &tmap_do,
-                          &bars.qdo_full[st.index], c * 64, h, q0);
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&bars.qdo_full[st.index], 2 * L::kTile);
+              for (int c = 0; c < D / 64; ++c) {
+                tma_load_3d(sQ + st.index * L::kTile + c * kBox, &tmap_q, &bars.qdo_full[st.index],
+                            c * 64, h, q0);
+                tma_load_3d(sDO + st.index * L::kTile + c * kBox, &tmap_do,
+                            &bars.qdo_full[st.index], c * 64, h, q0);
+              }
             }
+            // this q tile's lse (log2 domain; +inf for rows with no keys, so
+            // P = 0) and delta, four rows per lane, prefetched with the stage
+            float lv[4], dv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int qq = q0 + lane * 4 + u;
+              lv[u] = INFINITY;
+              dv[u] = 0.f;
+              if (qq < p.seqlen_q) {
+                const float raw = lse_h[qq];
+                lv[u] = raw == -INFINITY ? INFINITY : raw * kLog2e;
+                dv[u] = delta_h[qq];
+              }
+            }
+            reinterpret_cast<float4*>(s_lse + st.index * kBlockM)[lane] = make_float4(lv[0], lv[1], lv[2], lv[3]);
+            reinterpret_cast<float4*>(s_delta + st.index * kBlockM)[lane] = make_float4(dv[0], dv[1], dv[2], dv[3]);
+            mbar_arrive(&bars.qdo_full[st.index]);
             st.advance<kStages>();
           }
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0 && steps > 0) {
       constexpr uint32_t idesc_g = make_idesc_bf16(128, D, false, true);
       const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sDS);
@@ -274,13 +308,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t q_addr = smem_u32(sQ + gst.index * L::kTile);
         const uint32_t do_addr = smem_u32(sDO + gst.index * L::kTile);
 #pragma unroll
-        for (int k = 0; k < kBlockM / 16; ++k) {
+        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
           // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] MN-major
-          umma_bf16_ts(t_dv, t_dpt + k * 8, make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
+          umma_bf16_ts(t_dv, t_dpt + k * 8 + (k >= 4 ? 32 : 0), make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
 #pragma unroll
-        for (int k = 0; k < kBlockM / 16; ++k) {
+        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
           // dK += dS^T Q : A = dS^T [keys, q] K-major smem, B = Q [q, D] MN-major
           umma_bf16_ss(t_dk, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
                        make_smem_desc(q_addr + k * 16 * 128, kBox, 1024), idesc_g,
@@ -299,15 +333,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int row = warp * 32 + lane;
+    // two warpgroups split the 128 query columns of every step: wg 0 takes
+    // [0, 64), wg 1 [64, 128); both see all 128 key rows (TMEM lanes)
+    const int wg = warp / 4;
+    const int col0 = wg * 64;
+    const int row = (warp % 4) * 32 + lane;
     const int key = tile.k0 + row;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const float sl2 = p.scale_log2;
     int t = 0;
+    PipeState cst;  // Q / dO / lse / delta stage of the current step
     for (int g = 0; g < group; ++g) {
-      const int h = head_k * group + g;
-      const float* lse_h = p.lse + static_cast<size_t>(h) * p.seqlen_q;
-      const float* delta_h = p.delta + static_cast<size_t>(h) * p.seqlen_q;
       for (int it = tile.item_begin; it < tile.item_end; ++it) {
         const BwdItem item = p.k_items[it];
         // rows of this slice that may attend `key`: [qlo, qhi)
@@ -320,64 +356,87 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int i = 0; i < item.n_qtiles; ++i, ++t) {
           const int q0 = item.q_begin + i * kBlockM;
-          float* lse_b = s_lse;
-          float* delta_b = s_delta;
-          named_bar_sync(1, kMath);  // every math thread is done with the previous step's values
-          {
-            const int qq = q0 + row;
-            float l = INFINITY, dlt = 0.f;
-            if (qq < p.seqlen_q) {
-              const float raw = lse_h[qq];
-              l = raw == -INFINITY ? INFINITY : raw * kLog2e;
-              dlt = delta_h[qq];
-            }
-            lse_b[row] = l;
-            delta_b[row] = dlt;
-          }
-          named_bar_sync(1, kMath);
+          // lse / delta of this step were staged with its Q / dO tiles
+          const float* lse_s = s_lse + cst.index * kBlockM;
+          const float* delta_s = s_delta + cst.index * kBlockM;
+          mbar_wait(&bars.qdo_full[cst.index], cst.phase);
+          cst.advance<kStages>();
           mbar_wait(&bars.s_full, t & 1);
           tc_fence_after();
-          float pv[128];
-          {
-            uint32_t s[128];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
-              tmem_ld32(t_st + lane_off + c * 32, chunk);
-            }
-            tmem_ld_wait();
+          if (p.experiment == 1) {
             tc_fence_before();
             mbar_arrive(&bars.s_free);
-            const bool all_in = qlo <= q0 && q0 + kBlockM <= qhi;
+            mbar_wait(&bars.dp_full, t & 1);
+            tc_fence_before();
+            mbar_arrive(&bars.p_full);
+            continue;
+          }
+          float pv[64];
+          {
+            const float4* l4 = reinterpret_cast<const float4*>(lse_s + col0);
+            const int qb = q0 + col0;
+            const bool all_in = qlo <= qb && qb + 64 <= qhi;
 #pragma unroll
-            for (int c = 0; c < 128; ++c) {
-              const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_b[c]);
-              const float e = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
-              pv[c] = (all_in || (q0 + c >= qlo && q0 + c < qhi)) ? e : 0.f;
+            for (int h2 = 0; h2 < 2; ++h2) {
+              uint32_t s[32];
+              tmem_ld32(t_st + lane_off + col0 + h2 * 32, s);
+              tmem_ld_wait();
+              if (h2 == 1) {
+                tc_fence_before();
+                mbar_arrive(&bars.s_free);
+              }
+              if (all_in) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const float4 L = l4[h2 * 8 + c];
+                  const float lv[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const float x = fmaf(__uint_as_float(s[4 * c + u]), sl2, -lv[u]);
+                    pv[h2 * 32 + 4 * c + u] = u == 3 ? exp2_poly(x) : fast_exp2(x);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                  const float4 L = l4[h2 * 8 + c];
+                  const float lv[4] = {L.x, L.y, L.z, L.w};
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) {
+                    const int qq = qb + h2 * 32 + 4 * c + u;
+                    const float e = fast_exp2(fmaf(__uint_as_float(s[4 * c + u]), sl2, -lv[u]));
+                    pv[h2 * 32 + 4 * c + u] = (qq >= qlo && qq < qhi) ? e : 0.f;
+                  }
+                }
+              }
             }
           }
           mbar_wait(&bars.dp_full, t & 1);
           tc_fence_after();
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             uint32_t dp[32];
-            tmem_ld32(t_dpt + lane_off + c * 32, dp);
+            tmem_ld32(t_dpt + lane_off + col0 + c * 32, dp);
             tmem_ld_wait();
+            const float4* d4 = reinterpret_cast<const float4*>(delta_s + col0 + c * 32);
             uint32_t pk[16], ds[16];
 #pragma unroll
-            for (int j = 0; j < 32; j += 2) {
-              const int col = c * 32 + j;
-              pk[j / 2] = pack_bf16(pv[col], pv[col + 1]);
-              ds[j / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - delta_b[col]),
-                                    pv[col + 1] * (__uint_as_float(dp[j + 1]) - delta_b[col + 1]));
+            for (int j = 0; j < 8; ++j) {
+              const float4 dl = d4[j];
+              const int b = c * 32 + 4 * j;
+              pk[2 * j] = pack_bf16(pv[b], pv[b + 1]);
+              pk[2 * j + 1] = pack_bf16(pv[b + 2], pv[b + 3]);
+              ds[2 * j] = pack_bf16(pv[b] * (__uint_as_float(dp[4 * j]) - dl.x),
+                                    pv[b + 1] * (__uint_as_float(dp[4 * j + 1]) - dl.y));
+              ds[2 * j + 1] = pack_bf16(pv[b + 2] * (__uint_as_float(dp[4 * j + 2]) - dl.z),
+                                        pv[b + 3] * (__uint_as_float(dp[4 * j + 3]) - dl.w));
             }
-            // P^T chunk -> dP^T columns [c*16, c*16+16) (already consumed)
-            tmem_st16(t_dpt + lane_off + c * 16, pk);
-            // dS^T chunk -> smem row `row`, q columns [c*32, c*32+32)
+            // P^T chunk -> this warpgroup's consumed dP^T columns [col0 + c*16, +16)
+            tmem_st16(t_dpt + lane_off + col0 + c * 16, pk);
+            // dS^T chunk -> smem row `row`, q columns [col0 + c*32, +32) (box wg)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-              const int ch = c * 4 + u;
-              *reinterpret_cast<uint4*>(sDS + (ch / 8) * kBox + sw128_offset(row, ch % 8)) =
+              *reinterpret_cast<uint4*>(sDS + wg * kBox + sw128_offset(row, c * 4 + u)) =
                   make_uint4(ds[u * 4 + 0], ds[u * 4 + 1], ds[u * 4 + 2], ds[u * 4 + 3]);
             }
           }
@@ -395,13 +454,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool valid = key < p.seqlen_k;
     const size_t row_off = (static_cast<size_t>(key) * p.hk + head_k) * D;
     const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
-    epilogue_rows<D>(t_dv + lane_off, steps > 0, valid, p.dv, row_off, 1.f, f32, acc);
-    epilogue_rows<D>(t_dk + lane_off, steps > 0, valid, p.dk, row_off, p.scale, f32, acc);
+    if (wg == 0) {
+      epilogue_rows<D>(t_dv + lane_off, steps > 0, valid, p.dv, row_off, 1.f, f32, acc);
+    } else {
+      epilogue_rows<D>(t_dk + lane_off, steps > 0, valid, p.dk, row_off, p.scale, f32, acc);
+    }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -460,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(&bars.done, 1);
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<512>(&tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(&tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -473,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sV = smem + L::kV;
   uint8_t* sDS = smem + L::kDS;
 
-  if (warp == 4) {
+  if (warp == kTmaWarp) {
     if (lane == 0 && steps > 0) {
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
@@ -501,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == kMmaWarp) {
     if (lane == 0 && steps > 0) {
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, false, true);
       const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
@@ -530,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t k_addr = smem_u32(sK + gst.index * L::kTile);
 #pragma unroll
-        for (int k = 0; k < kBlockN / 16; ++k) {
+        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockN / 16); ++k) {
           // dQ += dS K : A = dS [q, keys] K-major, B = K [keys, D] MN-major
           umma_bf16_ss(t_dq, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
                        make_smem_desc(k_addr + k * 16 * 128, kBox, 1024), idesc_q,
@@ -549,9 +611,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int row = warp * 32 + lane;
+    // two warpgroups split the 128 key columns: wg 0 [0, 64), wg 1 [64, 128)
+    const int wg = warp / 4;
+    const int col0 = wg * 64;
+    const int row = (warp % 4) * 32 + lane;
     const int q = tile.q0 + row;
-    const uint32_t lane_off = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const bool valid = q < p.seqlen_q;
     const float sl2 = p.scale_log2;
     float lse_l2 = INFINITY, dlt = 0.f;
@@ -569,41 +634,57 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = item.k_begin + j * kBlockN;
         mbar_wait(&bars.s_full, t & 1);
         tc_fence_after();
-        float pv[128];
+        if (p.experiment == 1) {
+          tc_fence_before();
+          mbar_arrive(&bars.s_free);
+          mbar_wait(&bars.dp_full, t & 1);
+          tc_fence_before();
+          mbar_arrive(&bars.p_full);
+          continue;
+        }
+        float pv[64];
         {
-          uint32_t s[128];
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
-            tmem_ld32(t_s + lane_off + c * 32, chunk);
-          }
+          uint32_t s[64];
+          tmem_ld32(t_s + lane_off + col0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+          tmem_ld32(t_s + lane_off + col0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
           tmem_ld_wait();
           tc_fence_before();
           mbar_arrive(&bars.s_free);
-          const bool all_in = lo <= k0 && k0 + kBlockN <= hi;
+          const int kb = k0 + col0;
+          if (lo <= kb && kb + 64 <= hi) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c) {
-            const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
-            const float e = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
-            pv[c] = (all_in || (k0 + c >= lo && k0 + c < hi)) ? e : 0.f;
+            for (int c = 0; c < 64; ++c) {
+              const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
+              pv[c] = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+              const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
+              pv[c] = (kb + c >= lo && kb + c < hi) ? e : 0.f;
+            }
           }
         }
         mbar_wait(&bars.dp_full, t & 1);
         tc_fence_after();
-        uint32_t ds[64];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t dp[32];
-          tmem_ld32(t_dp + lane_off + c * 32, dp);
+        for (int c = 0; c < 2; ++c) {
+          uint32_t dp[32], ds[16];
+          tmem_ld32(t_dp + lane_off + col0 + c * 32, dp);
           tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; j += 2) {
             const int col = c * 32 + j;
-            ds[col / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - dlt),
-                                    pv[col + 1] * (__uint_as_float(dp[j + 1]) - dlt));
+            ds[j / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - dlt),
+                                  pv[col + 1] * (__uint_as_float(dp[j + 1]) - dlt));
+          }
+          // dS chunk -> smem row `row`, key columns [col0 + c*32, +32) (box wg)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            *reinterpret_cast<uint4*>(sDS + wg * kBox + sw128_offset(row, c * 4 + u)) =
+                make_uint4(ds[u * 4 + 0], ds[u * 4 + 1], ds[u * 4 + 2], ds[u * 4 + 3]);
           }
         }
-        store_row_sw128(sDS, row, ds);
         fence_proxy_async_smem();
         tc_fence_before();
         mbar_arrive(&bars.p_full);
@@ -613,14 +694,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars.done, 0);
       tc_fence_after();
     }
-    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D;
-    epilogue_rows<D>(t_dq + lane_off, steps > 0, valid, p.dq, row_off, p.scale, p.grad_f32 != 0,
-                     p.accumulate != 0);
+    // each warpgroup writes half of the dQ row
+    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + wg * (D / 2);
+    epilogue_rows<D / 2>(t_dq + lane_off + wg * (D / 2), steps > 0, valid, p.dq, row_off, p.scale,
+                         p.grad_f32 != 0, p.accumulate != 0);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -636,7 +718,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
   cudaError_t err = cudaSuccess;
   if ((parts & 1) && num_k_tiles > 0) {
-    const int smem = DkvSmem<D>::kBytes + 1024;
+    const int smem = DkvSmem<D>::kBytes;  // 1024-aligned dynamic window, barriers inside
     err = cudaFuncSetAttribute(ffa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
@@ -684,6 +766,10 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.dv = grad_v;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
+  {
+    const char* e = std::getenv("MAGI_BWD_EXPERIMENT");
+    prm.experiment = e ? std::atoi(e) : 0;
+  }
   if (head_dim == 128) return launch_bwd_impl<128>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
   if (head_dim == 64) return launch_bwd_impl<64>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
   return cudaErrorInvalidValue;
