@@ -61,9 +61,12 @@ struct BwdParams {
   void* dq;
   void* dk;
   void* dv;
+  const void* q;     // dQ kernel stages Q / dO rows into TMEM directly
+  const void* dout;
   int32_t grad_f32;
   int32_t accumulate;
   int32_t experiment;  // diagnostics: 1 = no elementwise work, 2 = no gradient MMAs
+  int32_t num_k_tiles, num_q_tiles;
 };
 
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
@@ -188,8 +191,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-byte alignment
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile_rank = blockIdx.x / p.hk;
-  const int head_k = blockIdx.x % p.hk;
+  // head-major grid: the CTAs running together share one key/value head, so
+  // the Q / dO tiles of its query-head group stay resident in L2
+  const int tile_rank = blockIdx.x % p.num_k_tiles;
+  const int head_k = blockIdx.x / p.num_k_tiles;
   const int group = p.hq / p.hk;
   const BwdTile tile = p.k_tiles[tile_rank];
   const int steps = tile.n_qtiles * group;
@@ -310,13 +315,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
           // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] MN-major
-          umma_bf16_ts(t_dv, t_dpt + k * 8 + (k >= 4 ? 32 : 0), make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
+          // q columns [16k, 16k+16) of P^T sit at (warpgroup k/4) * 64 +
+          // (chunk (k%4)/2) * 32 + (k%2) * 8 inside the dP^T region; dS^T 16 further
+          umma_bf16_ts(t_dv, t_dpt + (k >> 2) * 64 + ((k >> 1) & 1) * 32 + (k & 1) * 8,
+                       make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
 #pragma unroll
         for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
-          // dK += dS^T Q : A = dS^T [keys, q] K-major smem, B = Q [q, D] MN-major
-          umma_bf16_ss(t_dk, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
+          // dK += dS^T Q : A = dS^T (TMEM), B = Q [q, D] MN-major
+          umma_bf16_ts(t_dk, t_dpt + (k >> 2) * 64 + ((k >> 1) & 1) * 32 + (k & 1) * 8 + 16,
                        make_smem_desc(q_addr + k * 16 * 128, kBox, 1024), idesc_g,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
@@ -431,17 +439,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               ds[2 * j + 1] = pack_bf16(pv[b + 2] * (__uint_as_float(dp[4 * j + 2]) - dl.z),
                                         pv[b + 3] * (__uint_as_float(dp[4 * j + 3]) - dl.w));
             }
-            // P^T chunk -> this warpgroup's consumed dP^T columns [col0 + c*16, +16)
-            tmem_st16(t_dpt + lane_off + col0 + c * 16, pk);
-            // dS^T chunk -> smem row `row`, q columns [col0 + c*32, +32) (box wg)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              *reinterpret_cast<uint4*>(sDS + wg * kBox + sw128_offset(row, c * 4 + u)) =
-                  make_uint4(ds[u * 4 + 0], ds[u * 4 + 1], ds[u * 4 + 2], ds[u * 4 + 3]);
-            }
+            // P^T and dS^T (packed bf16) into the 32 dP^T columns this chunk
+            // just consumed: P^T in the first 16, dS^T in the next 16
+            tmem_st16(t_dpt + lane_off + col0 + c * 32, pk);
+            tmem_st16(t_dpt + lane_off + col0 + c * 32 + 16, ds);
           }
           tmem_st_wait();
-          fence_proxy_async_smem();
           tc_fence_before();
           mbar_arrive(&bars.p_full);
         }
@@ -470,22 +473,46 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // =========================================================================== dQ
+// All three MMAs take A from TMEM: Q and dO are staged into TMEM once per CTA
+// (packed bf16, thread = row), dS goes back into the consumed dP columns, so
+// shared memory only carries the streamed K / V tiles (B operands).
+// TMEM: S [0,128) dP [128,256) dQ [256,256+D) Q [384,384+D/2) dO [448,448+D/2).
 template <int D>
 struct DqSmem {
   static constexpr uint32_t kTile = (D / 64) * kBox;
-  static constexpr uint32_t kQ = 0;
-  static constexpr uint32_t kDO = kQ + kTile;
-  static constexpr uint32_t kK = kDO + kTile;             // kStages
-  static constexpr uint32_t kV = kK + kStages * kTile;    // kStages
-  static constexpr uint32_t kDS = kV + kStages * kTile;   // dS [q, keys] bf16
-  static constexpr uint32_t kBytes = kDS + 2 * kBox;
+  static constexpr int kKvStages = 3;
+  static constexpr uint32_t kK = 0;                       // kKvStages
+  static constexpr uint32_t kV = kK + kKvStages * kTile;  // kKvStages
+  static constexpr uint32_t kBytes = kV + kKvStages * kTile;
 };
 
 struct DqBarriers {
   uint64_t qdo_full;
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+  uint64_t k_full[3], k_empty[3], v_full[3], v_empty[3];
   uint64_t s_full, s_free, dp_full, p_full, done;
 };
+
+// Row `q` of a [tokens, heads, D] bf16 tensor -> this thread's TMEM lane,
+// packed pairs; the calling warpgroup stages D/2 columns starting at col0.
+template <int D>
+__device__ __forceinline__ void stage_row_to_tmem(const __nv_bfloat16* base, int hq, int head, int q,
+                                                  bool valid, int col0, uint32_t taddr) {
+  uint32_t v[32];
+  const uint4* src = reinterpret_cast<const uint4*>(base + (static_cast<size_t>(q) * hq + head) * D + col0);
+#pragma unroll
+  for (int c = 0; c < D / 16; ++c) {  // D/2 bf16 = D/16 x 16 B
+    const uint4 x = valid ? src[c] : make_uint4(0, 0, 0, 0);
+    v[4 * c + 0] = x.x;
+    v[4 * c + 1] = x.y;
+    v[4 * c + 2] = x.z;
+    v[4 * c + 3] = x.w;
+  }
+  if constexpr (D == 128) {
+    tmem_st32(taddr, v);
+  } else {
+    tmem_st16(taddr, v);
+  }
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -494,22 +521,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                       const __grid_constant__ CUtensorMap tmap_v,
                       const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
   using L = DqSmem<D>;
+  constexpr int S = L::kKvStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   __shared__ DqBarriers bars;
   __shared__ uint32_t tmem_slot;
+  (void)tmap_q;
+  (void)tmap_do;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile_rank = blockIdx.x / p.hq;
-  const int head = blockIdx.x % p.hq;
+  // head-major grid: co-running CTAs stream the same K / V (L2 resident)
+  const int tile_rank = blockIdx.x % p.num_q_tiles;
+  const int head = blockIdx.x / p.num_q_tiles;
   const int head_k = head / (p.hq / p.hk);
   const FwdTile tile = p.q_tiles[tile_rank];
   const int steps = tile.n_ktiles;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars.qdo_full, 1);
-    for (int s = 0; s < kStages; ++s) {
+    mbar_init(&bars.qdo_full, kMath);
+    for (int s = 0; s < S; ++s) {
       mbar_init(&bars.k_full[s], 1);
       mbar_init(&bars.k_empty[s], 1);
       mbar_init(&bars.v_full[s], 1);
@@ -528,22 +559,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   const uint32_t t_s = tmem, t_dp = tmem + 128, t_dq = tmem + 256;
+  const uint32_t t_q = tmem + 384, t_do = tmem + 448;
 
-  uint8_t* sQ = smem + L::kQ;
-  uint8_t* sDO = smem + L::kDO;
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
-  uint8_t* sDS = smem + L::kDS;
 
   if (warp == kTmaWarp) {
     if (lane == 0 && steps > 0) {
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
-      mbar_arrive_expect_tx(&bars.qdo_full, 2 * L::kTile);
-      for (int c = 0; c < D / 64; ++c) {
-        tma_load_3d(sQ + c * kBox, &tmap_q, &bars.qdo_full, c * 64, head, tile.q0);
-        tma_load_3d(sDO + c * kBox, &tmap_do, &bars.qdo_full, c * 64, head, tile.q0);
-      }
       PipeState st;
       for (int it = tile.item_begin; it < tile.item_end; ++it) {
         const FwdItem item = p.q_items[it];
@@ -559,25 +583,34 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < D / 64; ++c)
             tma_load_3d(sV + st.index * L::kTile + c * kBox, &tmap_v, &bars.v_full[st.index],
                         c * 64, head_k, k0);
-          st.advance<kStages>();
+          st.advance<S>();
         }
       }
     }
   } else if (warp == kMmaWarp) {
     if (lane == 0 && steps > 0) {
+      constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, false, true);
-      const uint32_t q_addr = smem_u32(sQ), do_addr = smem_u32(sDO), ds_addr = smem_u32(sDS);
+      // A = Q / dO from TMEM (k-step = 16 head-dim elements = 8 packed columns),
+      // B = K / V tile [keys, D] K-major from smem
+      auto issue_rows = [&](uint32_t d_tmem, uint32_t a_tmem, uint32_t b_addr) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k) {
+          umma_bf16_ts(d_tmem, a_tmem + k * 8,
+                       make_smem_desc(b_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
+        }
+      };
       mbar_wait(&bars.qdo_full, 0);
       PipeState nst, gst;
       mbar_wait(&bars.k_full[nst.index], nst.phase);
       mbar_wait(&bars.v_full[nst.index], nst.phase);
       tc_fence_after();
-      mma_rows_x_rows<D>(t_s, q_addr, smem_u32(sK + nst.index * L::kTile));
+      issue_rows(t_s, t_q, smem_u32(sK + nst.index * L::kTile));
       umma_commit(&bars.s_full);
-      mma_rows_x_rows<D>(t_dp, do_addr, smem_u32(sV + nst.index * L::kTile));
+      issue_rows(t_dp, t_do, smem_u32(sV + nst.index * L::kTile));
       umma_commit(&bars.dp_full);
       umma_commit(&bars.v_empty[nst.index]);
-      nst.advance<kStages>();
+      nst.advance<S>();
       for (int t = 0; t < steps; ++t) {
         const bool more = t + 1 < steps;
         if (more) {
@@ -585,7 +618,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars.k_full[nst.index], nst.phase);
           mbar_wait(&bars.v_full[nst.index], nst.phase);
           tc_fence_after();
-          mma_rows_x_rows<D>(t_s, q_addr, smem_u32(sK + nst.index * L::kTile));
+          issue_rows(t_s, t_q, smem_u32(sK + nst.index * L::kTile));
           umma_commit(&bars.s_full);
         }
         mbar_wait(&bars.p_full, t & 1);
@@ -593,18 +626,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t k_addr = smem_u32(sK + gst.index * L::kTile);
 #pragma unroll
         for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockN / 16); ++k) {
-          // dQ += dS K : A = dS [q, keys] K-major, B = K [keys, D] MN-major
-          umma_bf16_ss(t_dq, make_smem_desc(ds_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024),
+          // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys [0,64)
+          // at +0, keys [64,128) at +64), B = K [keys, D] MN-major
+          umma_bf16_ts(t_dq, t_dp + k * 8 + (k >= 4 ? 32 : 0),
                        make_smem_desc(k_addr + k * 16 * 128, kBox, 1024), idesc_q,
                        (t > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&bars.k_empty[gst.index]);
-        gst.advance<kStages>();
+        gst.advance<S>();
         if (more) {
-          mma_rows_x_rows<D>(t_dp, do_addr, smem_u32(sV + nst.index * L::kTile));
+          // dP(t+1) overwrites the dS columns read above: in-order pipe
+          issue_rows(t_dp, t_do, smem_u32(sV + nst.index * L::kTile));
           umma_commit(&bars.dp_full);
           umma_commit(&bars.v_empty[nst.index]);
-          nst.advance<kStages>();
+          nst.advance<S>();
         } else {
           umma_commit(&bars.done);
         }
@@ -619,6 +654,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const bool valid = q < p.seqlen_q;
     const float sl2 = p.scale_log2;
+    if (steps > 0) {
+      // stage Q and dO rows into TMEM (each warpgroup half of the head dim)
+      stage_row_to_tmem<D>(static_cast<const __nv_bfloat16*>(p.q), p.hq, head, q, valid,
+                           wg * (D / 2), t_q + lane_off + wg * (D / 4));
+      stage_row_to_tmem<D>(static_cast<const __nv_bfloat16*>(p.dout), p.hq, head, q, valid,
+                           wg * (D / 2), t_do + lane_off + wg * (D / 4));
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars.qdo_full);
+    }
     float lse_l2 = INFINITY, dlt = 0.f;
     if (valid) {
       const float raw = p.lse[static_cast<size_t>(head) * p.seqlen_q + q];
@@ -644,24 +689,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         float pv[64];
         {
-          uint32_t s[64];
-          tmem_ld32(t_s + lane_off + col0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-          tmem_ld32(t_s + lane_off + col0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-          tmem_ld_wait();
-          tc_fence_before();
-          mbar_arrive(&bars.s_free);
           const int kb = k0 + col0;
-          if (lo <= kb && kb + 64 <= hi) {
+          const bool all_in = lo <= kb && kb + 64 <= hi;
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-              const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
-              pv[c] = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t s[32];
+            tmem_ld32(t_s + lane_off + col0 + h2 * 32, s);
+            tmem_ld_wait();
+            if (h2 == 1) {
+              tc_fence_before();
+              mbar_arrive(&bars.s_free);
             }
-          } else {
+            if (all_in) {
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-              const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
-              pv[c] = (kb + c >= lo && kb + c < hi) ? e : 0.f;
+              for (int c = 0; c < 32; ++c) {
+                const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
+                pv[h2 * 32 + c] = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int kk = kb + h2 * 32 + c;
+                const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
+                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? e : 0.f;
+              }
             }
           }
         }
@@ -673,19 +724,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld32(t_dp + lane_off + col0 + c * 32, dp);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const int col = c * 32 + j;
-            ds[j / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j]) - dlt),
-                                  pv[col + 1] * (__uint_as_float(dp[j + 1]) - dlt));
+          for (int j2 = 0; j2 < 32; j2 += 2) {
+            const int col = c * 32 + j2;
+            ds[j2 / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j2]) - dlt),
+                                   pv[col + 1] * (__uint_as_float(dp[j2 + 1]) - dlt));
           }
-          // dS chunk -> smem row `row`, key columns [col0 + c*32, +32) (box wg)
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            *reinterpret_cast<uint4*>(sDS + wg * kBox + sw128_offset(row, c * 4 + u)) =
-                make_uint4(ds[u * 4 + 0], ds[u * 4 + 1], ds[u * 4 + 2], ds[u * 4 + 3]);
-          }
+          // dS chunk -> this warpgroup's consumed dP columns [col0 + c*16, +16)
+          tmem_st16(t_dp + lane_off + col0 + c * 16, ds);
         }
-        fence_proxy_async_smem();
+        tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.p_full);
       }
@@ -764,6 +811,10 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.dq = grad_q;
   prm.dk = grad_k;
   prm.dv = grad_v;
+  prm.q = q;
+  prm.num_k_tiles = num_k_tiles;
+  prm.num_q_tiles = num_q_tiles;
+  prm.dout = grad_out;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
   {

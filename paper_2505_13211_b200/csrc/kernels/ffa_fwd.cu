@@ -113,8 +113,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  const int tile_rank = blockIdx.x / p.hq;
-  const int head = blockIdx.x % p.hq;
+  // head-major grid: co-running CTAs stream the same K / V (L2 resident)
+  const int tile_rank = blockIdx.x % p.num_tiles;
+  const int head = blockIdx.x / p.num_tiles;
   const int head_k = head / (p.hq / p.hk);
   const FwdTile tile = p.tiles[tile_rank];
   const int n_total = tile.n_ktiles;
