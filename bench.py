@@ -277,24 +277,63 @@ def run_single(args) -> None:
     h2d = sum(t.numel() * t.element_size() for t in (q_h, k_h, v_h, do_h))
     d2h = sum(t.numel() * t.element_size() for t in (dq_h, dk_h, dv_h))
 
-    def e2e_step():
-        q.copy_(q_h, non_blocking=True)
-        k.copy_(k_h, non_blocking=True)
-        v.copy_(v_h, non_blocking=True)
-        do.copy_(do_h, non_blocking=True)
-        for _, fn, _ in parts:
-            fn()
-        dq_h.copy_(dq, non_blocking=True)
-        dk_h.copy_(dk, non_blocking=True)
-        dv_h.copy_(dv, non_blocking=True)
+    # Two device buffer sets so step i+1's inputs travel (H2D stream) and step
+    # i-1's gradients return (D2H stream) while step i computes. Every step
+    # still copies its own inputs in and its gradients out through PCIe.
+    sets = [dict(q=q, k=k, v=v, do=do, dq=dq, dk=dk, dv=dv)]
+    sets.append({n: torch.empty_like(t) for n, t in sets[0].items()})
+    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
-    e2e_step()
+    def step_on(b):
+        _lib.check(L.magiplan_ffa_fwd(plan.handle, b["q"].data_ptr(), b["k"].data_ptr(), b["v"].data_ptr(),
+                                      out.data_ptr(), lse.data_ptr(), hq, hk, scale, BF, 0, sp))
+        _lib.check(L.magiplan_ffa_bwd_preprocess(out.data_ptr(), b["do"].data_ptr(), delta.data_ptr(),
+                                                 S, hq, d, BF, sp))
+        _lib.check(L.magiplan_ffa_bwd_dkdv(plan.handle, b["q"].data_ptr(), b["k"].data_ptr(),
+                                           b["v"].data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                           b["do"].data_ptr(), b["dk"].data_ptr(), b["dv"].data_ptr(),
+                                           hq, hk, scale, BF, 0, sp))
+        _lib.check(L.magiplan_ffa_bwd_dq(plan.handle, b["q"].data_ptr(), b["k"].data_ptr(), b["v"].data_ptr(),
+                                         lse.data_ptr(), delta.data_ptr(), b["do"].data_ptr(),
+                                         b["dq"].data_ptr(), hq, hk, scale, BF, 0, sp))
+
+    def e2e_run(n):
+        mk = lambda: [torch.cuda.Event() for _ in range(n)]  # noqa: E731
+        ev_in, ev_done, ev_out = mk(), mk(), mk()
+
+        def h2d(i):
+            b = sets[i % 2]
+            with torch.cuda.stream(h2d_s):
+                if i >= 2:
+                    h2d_s.wait_event(ev_done[i - 2])  # step i-2 finished reading this set
+                for name, src in (("q", q_h), ("k", k_h), ("v", v_h), ("do", do_h)):
+                    b[name].copy_(src, non_blocking=True)
+                ev_in[i].record(h2d_s)
+
+        h2d(0)
+        for i in range(n):
+            if i + 1 < n:
+                h2d(i + 1)
+            stream.wait_event(ev_in[i])
+            if i >= 2:
+                stream.wait_event(ev_out[i - 2])  # gradients of this set already returned
+            step_on(sets[i % 2])
+            ev_done[i].record(stream)
+            with torch.cuda.stream(d2h_s):
+                d2h_s.wait_event(ev_done[i])
+                b = sets[i % 2]
+                dq_h.copy_(b["dq"], non_blocking=True)
+                dk_h.copy_(b["dk"], non_blocking=True)
+                dv_h.copy_(b["dv"], non_blocking=True)
+                ev_out[i].record(d2h_s)
+        stream.wait_event(ev_out[n - 1])
+
+    e2e_run(2)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
+    e2e_run(args.steps)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / args.steps
