@@ -58,11 +58,41 @@ def block_causal_area(seqlen: int, block: int) -> int:
     return n * (n + 1) // 2 * block * block
 
 
+def varlen_packed(seqlen: int, seed: int = 42, median: float = 2048.0, sigma: float = 1.0):
+    """BASELINE configs[3] / SURVEY §8d config 4: sample lengths from the
+    reference's deterministic log-normal generator (proj/src/pack.cpp:228-253,
+    reimplemented bit-exactly in the planner), taken in order until they cover
+    `seqlen`, the last one clipped; even samples FULL, odd samples CAUSAL."""
+    from paper_2505_13211_b200.planner import lognormal_lengths
+
+    lens, total, n = [], 0, 64
+    while total < seqlen:
+        lens = lognormal_lengths(n, median, sigma, seqlen, seed)
+        total = sum(lens)
+        n *= 2
+    out, acc = [], 0
+    for x in lens:
+        x = min(x, seqlen - acc)
+        out.append(x)
+        acc += x
+        if acc == seqlen:
+            break
+    qr, kr, ty, off = [], [], [], 0
+    for i, n_ in enumerate(out):
+        qr.append([off, off + n_])
+        kr.append([off, off + n_])
+        ty.append(0 if i % 2 == 0 else 1)
+        off += n_
+    return qr, kr, ty
+
+
 WORKLOADS = {
     # BASELINE.json configs[1]
     "magi1_4.5b_layer_s32k_b4096": dict(seqlen=32768, hq=24, hk=8, d=128, block=4096),
     # BASELINE.json configs[2]
     "magi1_24b_layer_s32k_b4096": dict(seqlen=32768, hq=48, hk=8, d=128, block=4096),
+    # BASELINE.json configs[3]: varlen packed FULL/CAUSAL clips
+    "varlen_packed_s32k": dict(seqlen=32768, hq=48, hk=8, d=128, block=4096, varlen=True),
 }
 DEFAULT_WORKLOAD = "magi1_4.5b_layer_s32k_b4096"
 
@@ -197,10 +227,16 @@ def run_single(args) -> None:
     S, hq, hk, d, block = wl["seqlen"], wl["hq"], wl["hk"], wl["d"], wl["block"]
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    qr, kr, ty = block_causal(S, block)
+    if wl.get("varlen"):
+        qr, kr, ty = varlen_packed(S)
+        mask_desc = f"varlen packed FULL/CAUSAL, {len(qr)} samples (lognormal median 2048, sigma 1, seed 42)"
+    else:
+        qr, kr, ty = block_causal(S, block)
+        mask_desc = f"block_causal(block={block})"
     plan = FFAPlan(qr, kr, ty, S, S, d)
     area = plan.area()
-    assert area == block_causal_area(S, block)
+    if not wl.get("varlen"):
+        assert area == block_causal_area(S, block)
     fwd_flops = 4 * area * hq * d
     bwd_flops = fwd_flops * 5 // 2
     step_flops = fwd_flops + bwd_flops
@@ -362,7 +398,7 @@ def run_single(args) -> None:
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {"workload": args.workload, "seqlen": S, "num_heads_q": hq, "num_heads_k": hk,
-                   "head_dim": d, "mask": f"block_causal(block={block})", "area_multiplicity": area,
+                   "head_dim": d, "mask": mask_desc, "area_multiplicity": area,
                    "flops_per_step": step_flops, "parallelism": "single GPU",
                    "l2": f"inputs larger than L2 (q {q.numel() * 2 / 1e6:.0f} MB, "
                          f"dO {do.numel() * 2 / 1e6:.0f} MB > 126 MB); no flush"},

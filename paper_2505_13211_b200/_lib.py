@@ -50,6 +50,7 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_cast_f32_bf16": (C.c_int, [_vp, _vp, _i64, _vp]),
     "magiplan_debug_umma_tile": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),
     "magiplan_debug_eval": (C.c_int, [_cp, C.POINTER(_vp)]),
+    "magiplan_debug_set_trace": (C.c_int, [_vp, _i32]),
 }
 
 

@@ -34,6 +34,7 @@ cudaError_t launch_range_scatter_add_f32(const float* src, float* dst, const int
                                          int64_t total_rows, int64_t row_elems,
                                          cudaStream_t stream);
 cudaError_t launch_cast_f32_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
+void set_bwd_trace(long long* buffer, int block);
 }  // namespace magi
 
 struct magiplan_ffa_plan {
@@ -261,6 +262,11 @@ magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
     if (n < 0) throw UsageError("n must be >= 0");
     cuda_check(magi::launch_cast_f32_bf16(src, dst, n, as_stream(cuda_stream)), "cast launch");
   });
+}
+
+magiplan_status magiplan_debug_set_trace(void* device_buffer, int32_t block) {
+  magi::set_bwd_trace(static_cast<long long*>(device_buffer), block);
+  return MAGIPLAN_OK;
 }
 
 magiplan_status magiplan_debug_umma_tile(const void* a, const void* b, float* c,

@@ -67,7 +67,25 @@ struct BwdParams {
   int32_t accumulate;
   int32_t experiment;  // diagnostics: 1 = no elementwise work, 2 = no gradient MMAs
   int32_t num_k_tiles, num_q_tiles;
+  long long* trace;     // diagnostics: event log of one CTA (nullptr = off)
+  int32_t trace_block;
 };
+
+long long* g_trace = nullptr;
+int g_trace_block = 0;
+
+// Event log record {event, step, %globaltimer ns} of the traced CTA.
+__device__ __forceinline__ void trace_event(long long* tr, int ev, int t) {
+  if (tr == nullptr) return;
+  unsigned long long ns;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+  const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tr), 1ull);
+  if (i < 20000) {
+    tr[1 + 3 * i] = ev;
+    tr[2 + 3 * i] = t;
+    tr[3 + 3 * i] = static_cast<long long>(ns);
+  }
+}
 
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
                                           int c, float scale, bool f32, bool accumulate) {
@@ -198,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int group = p.hq / p.hk;
   const BwdTile tile = p.k_tiles[tile_rank];
   const int steps = tile.n_qtiles * group;
+  long long* const tr = (static_cast<int>(blockIdx.x) == p.trace_block && lane == 0) ? p.trace : nullptr;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.kv_full, 1);
@@ -303,12 +322,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (more) {
           // S(t+1) as soon as S(t) is in registers
           mbar_wait(&bars.s_free, t & 1);
+          trace_event(tr, 1, t);
           mbar_wait(&bars.qdo_full[nst.index], nst.phase);
+          trace_event(tr, 2, t);
           tc_fence_after();
           mma_rows_x_rows<D>(t_st, k_addr, smem_u32(sQ + nst.index * L::kTile));
           umma_commit(&bars.s_full);
         }
         mbar_wait(&bars.p_full, t & 1);
+        trace_event(tr, 3, t);
         tc_fence_after();
         const uint32_t q_addr = smem_u32(sQ + gst.index * L::kTile);
         const uint32_t do_addr = smem_u32(sDO + gst.index * L::kTile);
@@ -367,9 +389,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           // lse / delta of this step were staged with its Q / dO tiles
           const float* lse_s = s_lse + cst.index * kBlockM;
           const float* delta_s = s_delta + cst.index * kBlockM;
+          long long* const trw = (warp % 4 == 0) ? tr : nullptr;  // one warp per warpgroup
           mbar_wait(&bars.qdo_full[cst.index], cst.phase);
           cst.advance<kStages>();
           mbar_wait(&bars.s_full, t & 1);
+          trace_event(trw, 10 + 10 * wg, t);
           tc_fence_after();
           if (p.experiment == 1) {
             tc_fence_before();
@@ -419,7 +443,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               }
             }
           }
+          trace_event(trw, 11 + 10 * wg, t);
           mbar_wait(&bars.dp_full, t & 1);
+          trace_event(trw, 12 + 10 * wg, t);
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -447,6 +473,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_st_wait();
           tc_fence_before();
           mbar_arrive(&bars.p_full);
+          trace_event(trw, 13 + 10 * wg, t);
         }
       }
     }
@@ -814,6 +841,8 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.q = q;
   prm.num_k_tiles = num_k_tiles;
   prm.num_q_tiles = num_q_tiles;
+  prm.trace = g_trace;
+  prm.trace_block = g_trace_block;
   prm.dout = grad_out;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
@@ -826,4 +855,13 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   return cudaErrorInvalidValue;
 }
 
+}  // namespace magi
+
+namespace magi {
+// Diagnostics: route one backward CTA's event log to a device buffer
+// (int64: [0] = record count, then {event, step, ns} triples); nullptr = off.
+void set_bwd_trace(long long* buffer, int block) {
+  g_trace = buffer;
+  g_trace_block = block;
+}
 }  // namespace magi
