@@ -34,7 +34,7 @@ def _sources() -> list[Path]:
 
 
 def _headers_mtime() -> float:
-    hdrs = list(CSRC.rglob("*.h")) + list(CSRC.rglob("*.hpp")) + list(CSRC.rglob("*.cuh"))
+    hdrs = [*CSRC.rglob("*.h"), *CSRC.rglob("*.hpp"), *CSRC.rglob("*.cuh"), *CSRC.rglob("*.inc")]
     hdrs += list((ROOT / "include").rglob("*.h"))
     return max((h.stat().st_mtime for h in hdrs), default=0.0)
 

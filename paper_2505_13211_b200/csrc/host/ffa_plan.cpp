@@ -210,7 +210,10 @@ void build_kmajor(FfaPlan& plan) {
         bounds(s, mid, l, h);
         if (h > k0) hi_q = mid; else lo_q = mid + 1;
       }
-      const int64_t qa = lo_q;
+      // start on a multiple of 4 rows: the dK/dV kernel fetches the tile's
+      // lse / delta rows by TMA, whose innermost coordinate must be 16-byte
+      // aligned (the extra rows fall outside the slice and are masked)
+      const int64_t qa = lo_q & ~int64_t{3};
       // last row whose lo < k1 (lo non-decreasing): first row with lo >= k1, minus one
       lo_q = s.qs;
       hi_q = s.qe;

@@ -67,6 +67,7 @@ struct BwdParams {
   int32_t accumulate;
   int32_t experiment;  // diagnostics: 1 = no elementwise work, 2 = no gradient MMAs
   int32_t num_k_tiles, num_q_tiles;
+  int32_t lse_tma;      // lse / delta rows fetched by TMA (row stride 16B-aligned)
   long long* trace;     // diagnostics: event log of one CTA (nullptr = off)
   int32_t trace_block;
 };
@@ -170,334 +171,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* v) {
       : "memory");
 }
 
-// =========================================================================== dK / dV
-template <int D>
-struct DkvSmem {
-  static constexpr uint32_t kTile = (D / 64) * kBox;
-  static constexpr uint32_t kK = 0;
-  static constexpr uint32_t kV = kK + kTile;
-  static constexpr uint32_t kQ = kV + kTile;               // kStages
-  static constexpr uint32_t kDO = kQ + kStages * kTile;    // kStages
-  static constexpr uint32_t kDS = kDO + kStages * kTile;   // dS^T [128 keys, 128 q] bf16
-  static constexpr uint32_t kLse = kDS + 2 * kBox;         // kStages x [128] f32 (log2 domain)
-  static constexpr uint32_t kDelta = kLse + kStages * kBlockM * 4;
-  static constexpr uint32_t kBars = kDelta + kStages * kBlockM * 4;
-  static constexpr uint32_t kBytes = kBars + 128;          // barriers + TMEM slot
-};
-
-// Lives in dynamic shared memory right after the tiles: with no static
-// shared memory the 1024-aligned dynamic window starts at offset 0, which is
-// what lets 227 KB of tiles fit without an alignment slack.
-struct DkvBarriers {
-  uint64_t kv_full;
-  uint64_t qdo_full[kStages], qdo_empty[kStages];
-  uint64_t s_full, s_free, dp_full, p_full, done;
-  uint32_t tmem_slot;
-};
-static_assert(sizeof(DkvBarriers) <= 128, "barrier block");
-
-template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
-    ffa_bwd_dkdv_kernel(const __grid_constant__ CUtensorMap tmap_q,
-                        const __grid_constant__ CUtensorMap tmap_k,
-                        const __grid_constant__ CUtensorMap tmap_v,
-                        const __grid_constant__ CUtensorMap tmap_do, const BwdParams p) {
-  using L = DkvSmem<D>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  DkvBarriers& bars = *reinterpret_cast<DkvBarriers*>(smem + L::kBars);
-  uint32_t& tmem_slot = bars.tmem_slot;
-  if ((smem_u32(smem) & 1023u) != 0) __trap();  // SW128 tiles need 1024-byte alignment
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // head-major grid: the CTAs running together share one key/value head, so
-  // the Q / dO tiles of its query-head group stay resident in L2
-  const int tile_rank = blockIdx.x % p.num_k_tiles;
-  const int head_k = blockIdx.x / p.num_k_tiles;
-  const int group = p.hq / p.hk;
-  const BwdTile tile = p.k_tiles[tile_rank];
-  const int steps = tile.n_qtiles * group;
-  long long* const tr = (static_cast<int>(blockIdx.x) == p.trace_block && lane == 0) ? p.trace : nullptr;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bars.kv_full, 1);
-    for (int s = 0; s < kStages; ++s) {
-      // TMA bytes (lane 0's expect_tx arrival) + one arrival per producer lane
-      // after it stored the stage's lse / delta
-      mbar_init(&bars.qdo_full[s], 1 + 32);
-      mbar_init(&bars.qdo_empty[s], 1);
-    }
-    mbar_init(&bars.s_full, 1);
-    mbar_init(&bars.s_free, kMath);
-    mbar_init(&bars.dp_full, 1);
-    mbar_init(&bars.p_full, kMath);
-    mbar_init(&bars.done, 1);
-    fence_barrier_init();
-  }
-  if (warp == kMmaWarp) tmem_alloc<512>(&tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = tmem_slot;
-  const uint32_t t_st = tmem;            // S^T
-  const uint32_t t_dpt = tmem + 128;     // dP^T, then P^T packed in its first 64 columns
-  const uint32_t t_dv = tmem + 256;      // dV [keys, D]
-  const uint32_t t_dk = tmem + 256 + D;  // dK [keys, D]
-
-  uint8_t* sK = smem + L::kK;
-  uint8_t* sV = smem + L::kV;
-  uint8_t* sQ = smem + L::kQ;
-  uint8_t* sDO = smem + L::kDO;
-  uint8_t* sDS = smem + L::kDS;
-  float* s_lse = reinterpret_cast<float*>(smem + L::kLse);
-  float* s_delta = reinterpret_cast<float*>(smem + L::kDelta);
-
-  if (warp == kTmaWarp) {
-    if (steps > 0) {
-      if (lane == 0) {
-        tma_prefetch_desc(&tmap_q);
-        tma_prefetch_desc(&tmap_do);
-        mbar_arrive_expect_tx(&bars.kv_full, 2 * L::kTile);
-        for (int c = 0; c < D / 64; ++c) {
-          tma_load_3d(sK + c * kBox, &tmap_k, &bars.kv_full, c * 64, head_k, tile.k0);
-          tma_load_3d(sV + c * kBox, &tmap_v, &bars.kv_full, c * 64, head_k, tile.k0);
-        }
-      }
-      PipeState st;
-      for (int g = 0; g < group; ++g) {
-        const int h = head_k * group + g;
-        const float* lse_h = p.lse + static_cast<size_t>(h) * p.seqlen_q;
-        const float* delta_h = p.delta + static_cast<size_t>(h) * p.seqlen_q;
-        for (int it = tile.item_begin; it < tile.item_end; ++it) {
-          const BwdItem item = p.k_items[it];
-          for (int i = 0; i < item.n_qtiles; ++i) {
-            const int q0 = item.q_begin + i * kBlockM;
-            mbar_wait(&bars.qdo_empty[st.index], st.phase ^ 1);
-            if (lane == 0) {
-              mbar_arrive_expect_tx(&bars.qdo_full[st.index], 2 * L::kTile);
-              for (int c = 0; c < D / 64; ++c) {
-                tma_load_3d(sQ + st.index * L::kTile + c * kBox, &tmap_q, &bars.qdo_full[st.index],
-                            c * 64, h, q0);
-                tma_load_3d(sDO + st.index * L::kTile + c * kBox, &tmap_do,
-                            &bars.qdo_full[st.index], c * 64, h, q0);
-              }
-            }
-            // this q tile's lse (log2 domain; +inf for rows with no keys, so
-            // P = 0) and delta, four rows per lane, prefetched with the stage
-            float lv[4], dv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int qq = q0 + lane * 4 + u;
-              lv[u] = INFINITY;
-              dv[u] = 0.f;
-              if (qq < p.seqlen_q) {
-                const float raw = lse_h[qq];
-                lv[u] = raw == -INFINITY ? INFINITY : raw * kLog2e;
-                dv[u] = delta_h[qq];
-              }
-            }
-            reinterpret_cast<float4*>(s_lse + st.index * kBlockM)[lane] = make_float4(lv[0], lv[1], lv[2], lv[3]);
-            reinterpret_cast<float4*>(s_delta + st.index * kBlockM)[lane] = make_float4(dv[0], dv[1], dv[2], dv[3]);
-            mbar_arrive(&bars.qdo_full[st.index]);
-            st.advance<kStages>();
-          }
-        }
-      }
-    }
-  } else if (warp == kMmaWarp) {
-    if (lane == 0 && steps > 0) {
-      constexpr uint32_t idesc_g = make_idesc_bf16(128, D, false, true);
-      const uint32_t k_addr = smem_u32(sK), v_addr = smem_u32(sV), ds_addr = smem_u32(sDS);
-      mbar_wait(&bars.kv_full, 0);
-      PipeState nst;  // stage of the next S / dP issue
-      PipeState gst;  // stage of the gradient MMAs
-      mbar_wait(&bars.qdo_full[nst.index], nst.phase);
-      tc_fence_after();
-      mma_rows_x_rows<D>(t_st, k_addr, smem_u32(sQ + nst.index * L::kTile));
-      umma_commit(&bars.s_full);
-      mma_rows_x_rows<D>(t_dpt, v_addr, smem_u32(sDO + nst.index * L::kTile));
-      umma_commit(&bars.dp_full);
-      nst.advance<kStages>();
-      for (int t = 0; t < steps; ++t) {
-        const bool more = t + 1 < steps;
-        if (more) {
-          // S(t+1) as soon as S(t) is in registers
-          mbar_wait(&bars.s_free, t & 1);
-          trace_event(tr, 1, t);
-          mbar_wait(&bars.qdo_full[nst.index], nst.phase);
-          trace_event(tr, 2, t);
-          tc_fence_after();
-          mma_rows_x_rows<D>(t_st, k_addr, smem_u32(sQ + nst.index * L::kTile));
-          umma_commit(&bars.s_full);
-        }
-        mbar_wait(&bars.p_full, t & 1);
-        trace_event(tr, 3, t);
-        tc_fence_after();
-        const uint32_t q_addr = smem_u32(sQ + gst.index * L::kTile);
-        const uint32_t do_addr = smem_u32(sDO + gst.index * L::kTile);
-#pragma unroll
-        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
-          // dV += P^T dO : A = P^T (TMEM, packed bf16), B = dO [q, D] MN-major
-          // q columns [16k, 16k+16) of P^T sit at (warpgroup k/4) * 64 +
-          // (chunk (k%4)/2) * 32 + (k%2) * 8 inside the dP^T region; dS^T 16 further
-          umma_bf16_ts(t_dv, t_dpt + (k >> 2) * 64 + ((k >> 1) & 1) * 32 + (k & 1) * 8,
-                       make_smem_desc(do_addr + k * 16 * 128, kBox, 1024), idesc_g,
-                       (t > 0 || k > 0) ? 1u : 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockM / 16); ++k) {
-          // dK += dS^T Q : A = dS^T (TMEM), B = Q [q, D] MN-major
-          umma_bf16_ts(t_dk, t_dpt + (k >> 2) * 64 + ((k >> 1) & 1) * 32 + (k & 1) * 8 + 16,
-                       make_smem_desc(q_addr + k * 16 * 128, kBox, 1024), idesc_g,
-                       (t > 0 || k > 0) ? 1u : 0u);
-        }
-        umma_commit(&bars.qdo_empty[gst.index]);
-        gst.advance<kStages>();
-        if (more) {
-          // dP(t+1) into the columns the gradient MMAs above read (in-order pipe)
-          mma_rows_x_rows<D>(t_dpt, v_addr, smem_u32(sDO + nst.index * L::kTile));
-          umma_commit(&bars.dp_full);
-          nst.advance<kStages>();
-        } else {
-          umma_commit(&bars.done);
-        }
-      }
-    }
-  } else {
-    // two warpgroups split the 128 query columns of every step: wg 0 takes
-    // [0, 64), wg 1 [64, 128); both see all 128 key rows (TMEM lanes)
-    const int wg = warp / 4;
-    const int col0 = wg * 64;
-    const int row = (warp % 4) * 32 + lane;
-    const int key = tile.k0 + row;
-    const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    const float sl2 = p.scale_log2;
-    int t = 0;
-    PipeState cst;  // Q / dO / lse / delta stage of the current step
-    for (int g = 0; g < group; ++g) {
-      for (int it = tile.item_begin; it < tile.item_end; ++it) {
-        const BwdItem item = p.k_items[it];
-        // rows of this slice that may attend `key`: [qlo, qhi)
-        int qlo = item.qs, qhi = item.qe;
-        if (key < item.ks || key >= item.ke) {
-          qhi = qlo;
-        } else {
-          if (item.type == kCausal || item.type == kBiCausal) qlo = max(qlo, key - (item.ke - item.qe));
-          if (item.type == kInvCausal || item.type == kBiCausal) qhi = min(qhi, key - item.ks + item.qs + 1);
-        }
-        for (int i = 0; i < item.n_qtiles; ++i, ++t) {
-          const int q0 = item.q_begin + i * kBlockM;
-          // lse / delta of this step were staged with its Q / dO tiles
-          const float* lse_s = s_lse + cst.index * kBlockM;
-          const float* delta_s = s_delta + cst.index * kBlockM;
-          long long* const trw = (warp % 4 == 0) ? tr : nullptr;  // one warp per warpgroup
-          mbar_wait(&bars.qdo_full[cst.index], cst.phase);
-          cst.advance<kStages>();
-          mbar_wait(&bars.s_full, t & 1);
-          trace_event(trw, 10 + 10 * wg, t);
-          tc_fence_after();
-          if (p.experiment == 1) {
-            tc_fence_before();
-            mbar_arrive(&bars.s_free);
-            mbar_wait(&bars.dp_full, t & 1);
-            tc_fence_before();
-            mbar_arrive(&bars.p_full);
-            continue;
-          }
-          float pv[64];
-          {
-            const float4* l4 = reinterpret_cast<const float4*>(lse_s + col0);
-            const int qb = q0 + col0;
-            const bool all_in = qlo <= qb && qb + 64 <= qhi;
-#pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-              uint32_t s[32];
-              tmem_ld32(t_st + lane_off + col0 + h2 * 32, s);
-              tmem_ld_wait();
-              if (h2 == 1) {
-                tc_fence_before();
-                mbar_arrive(&bars.s_free);
-              }
-              if (all_in) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                  const float4 L = l4[h2 * 8 + c];
-                  const float lv[4] = {L.x, L.y, L.z, L.w};
-#pragma unroll
-                  for (int u = 0; u < 4; ++u) {
-                    const float x = fmaf(__uint_as_float(s[4 * c + u]), sl2, -lv[u]);
-                    pv[h2 * 32 + 4 * c + u] = u == 3 ? exp2_poly(x) : fast_exp2(x);
-                  }
-                }
-              } else {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                  const float4 L = l4[h2 * 8 + c];
-                  const float lv[4] = {L.x, L.y, L.z, L.w};
-#pragma unroll
-                  for (int u = 0; u < 4; ++u) {
-                    const int qq = qb + h2 * 32 + 4 * c + u;
-                    const float e = fast_exp2(fmaf(__uint_as_float(s[4 * c + u]), sl2, -lv[u]));
-                    pv[h2 * 32 + 4 * c + u] = (qq >= qlo && qq < qhi) ? e : 0.f;
-                  }
-                }
-              }
-            }
-          }
-          trace_event(trw, 11 + 10 * wg, t);
-          mbar_wait(&bars.dp_full, t & 1);
-          trace_event(trw, 12 + 10 * wg, t);
-          tc_fence_after();
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t dp[32];
-            tmem_ld32(t_dpt + lane_off + col0 + c * 32, dp);
-            tmem_ld_wait();
-            const float4* d4 = reinterpret_cast<const float4*>(delta_s + col0 + c * 32);
-            uint32_t pk[16], ds[16];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 dl = d4[j];
-              const int b = c * 32 + 4 * j;
-              pk[2 * j] = pack_bf16(pv[b], pv[b + 1]);
-              pk[2 * j + 1] = pack_bf16(pv[b + 2], pv[b + 3]);
-              ds[2 * j] = pack_bf16(pv[b] * (__uint_as_float(dp[4 * j]) - dl.x),
-                                    pv[b + 1] * (__uint_as_float(dp[4 * j + 1]) - dl.y));
-              ds[2 * j + 1] = pack_bf16(pv[b + 2] * (__uint_as_float(dp[4 * j + 2]) - dl.z),
-                                        pv[b + 3] * (__uint_as_float(dp[4 * j + 3]) - dl.w));
-            }
-            // P^T and dS^T (packed bf16) into the 32 dP^T columns this chunk
-            // just consumed: P^T in the first 16, dS^T in the next 16
-            tmem_st16(t_dpt + lane_off + col0 + c * 32, pk);
-            tmem_st16(t_dpt + lane_off + col0 + c * 32 + 16, ds);
-          }
-          tmem_st_wait();
-          tc_fence_before();
-          mbar_arrive(&bars.p_full);
-          trace_event(trw, 13 + 10 * wg, t);
-        }
-      }
-    }
-    if (steps > 0) {
-      mbar_wait(&bars.done, 0);
-      tc_fence_after();
-    }
-    const bool valid = key < p.seqlen_k;
-    const size_t row_off = (static_cast<size_t>(key) * p.hk + head_k) * D;
-    const bool f32 = p.grad_f32 != 0, acc = p.accumulate != 0;
-    if (wg == 0) {
-      epilogue_rows<D>(t_dv + lane_off, steps > 0, valid, p.dv, row_off, 1.f, f32, acc);
-    } else {
-      epilogue_rows<D>(t_dk + lane_off, steps > 0, valid, p.dk, row_off, p.scale, f32, acc);
-    }
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    tmem_dealloc<512>(tmem);
-  }
-}
+#include "ffa_bwd_dkdv.inc"
 
 // =========================================================================== dQ
 // All three MMAs take A from TMEM: Q and dO are staged into TMEM once per CTA
@@ -796,8 +470,15 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
     err = cudaFuncSetAttribute(ffa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
-    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kThreads, smem, stream>>>(tq, tk, tv, tdo,
-                                                                                   prm);
+    BwdParams pk = prm;
+    pk.lse_tma = (prm.seqlen_q % 4) == 0;
+    CUtensorMap tl{}, td{};
+    if (pk.lse_tma) {
+      tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
+      td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
+    }
+    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
+                                                                                   td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

@@ -45,6 +45,27 @@ inline CUtensorMap make_tmap_bf16(const void* base, int rank, const uint64_t* di
   return map;
 }
 
+// [rows, cols] f32 matrix (row stride cols * 4 bytes, must be a multiple of
+// 16), box = box_cols x 1, no swizzle. Used for per-row lse / delta vectors.
+inline CUtensorMap make_tmap_f32_rows(const void* base, uint64_t rows, uint64_t cols,
+                                      uint32_t box_cols) {
+  CUtensorMap map;
+  const uint64_t dims[2] = {cols, rows};
+  const uint64_t strides[1] = {cols * 4};
+  const uint32_t box[2] = {box_cols, 1};
+  const uint32_t elem_strides[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(
+      &map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+      reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides),
+      reinterpret_cast<const cuuint32_t*>(box), elem_strides, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    throw std::runtime_error("cuTensorMapEncodeTiled (f32 rows) failed with code " + std::to_string(r));
+  }
+  return map;
+}
+
 // [tokens, heads, dim] token-major bf16 tensor viewed as 3-D (dim, heads, tokens);
 // one box = box_rows tokens x 64 dims of one head.
 inline CUtensorMap make_tmap_thd(const void* base, int64_t tokens, int64_t heads, int64_t dim,

@@ -1,10 +1,9 @@
 """Timeline of one dK/dV CTA (diagnostics; see magiplan_debug_set_trace).
 
-Events (globaltimer ns): MMA warp 1 = S(t+1) slot free, 2 = Q/dO(t+1) landed,
-3 = P/dS(t) ready; warpgroup w (10*w+10..13): S(t) ready, exp done, dP(t)
-ready, P/dS(t) written.
+Per-role logs (globaltimer ns): MMA 1 = S slot free, 2 = Q(t+1) landed,
+3 = P/dS(t) ready, 4 = dO(t+1) landed; warpgroups 10..13 = S(t) ready, exp
+done, dP(t) ready, P/dS(t) written; TMA 30 / 31 = Q / dO slot for step t free.
 """
-import math
 import statistics
 import sys
 
@@ -13,6 +12,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2505_13211_b200 import _lib  # noqa: E402
 from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward  # noqa: E402
+
+CAP = 8000
 
 
 def main(block: int = 0):
@@ -26,37 +27,35 @@ def main(block: int = 0):
     do = torch.randn(S, hq, d, device="cuda", dtype=torch.bfloat16)
     out, lse = ffa_forward(plan, q, k, v)
     ffa_backward(plan, q, k, v, out, lse, do)
-    buf = torch.zeros(1 + 3 * 20000, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(1 + 4 * 2 * CAP, dtype=torch.int64, device="cuda")
     _lib.check(_lib.lib().magiplan_debug_set_trace(buf.data_ptr(), block))
     ffa_backward(plan, q, k, v, out, lse, do)
     torch.cuda.synchronize()
     _lib.check(_lib.lib().magiplan_debug_set_trace(None, 0))
-    n = int(buf[0])
-    rec = buf[1:1 + 3 * min(n, 20000)].view(-1, 3).cpu().tolist()
+    data = buf[1:].view(4, CAP, 2).cpu().tolist()
     ev = {}
-    for e, t, ns in rec:
-        ev.setdefault((e, t), ns)
+    for role in range(4):
+        for key, ns in data[role]:
+            if ns == 0:
+                break
+            ev.setdefault((key >> 32, key & 0xFFFFFFFF), ns)
     steps = max(t for _, t in ev) + 1
-    t0 = min(ns for ns in ev.values())
+    t0 = min(ev.values())
 
-    def gap(a, b, ta_off=0):
-        out = []
-        for t in range(1, steps - 1):
-            if (a, t + ta_off) in ev and (b, t) in ev:
-                out.append(ev[(b, t)] - ev[(a, t + ta_off)])
-        return statistics.median(out) if out else float("nan")
+    def gap(a, b, off=0):
+        xs = [ev[(b, t)] - ev[(a, t + off)] for t in range(2, steps - 2) if (a, t + off) in ev and (b, t) in ev]
+        return statistics.median(xs) if xs else float("nan")
 
-    print(f"block {block}: {n} records, {steps} steps, span {(max(ev.values()) - t0) / 1e3:.1f} us")
-    per = [ev[(3, t + 1)] - ev[(3, t)] for t in range(1, steps - 2) if (3, t + 1) in ev and (3, t) in ev]
-    print(f"step period (P ready -> next P ready): median {statistics.median(per):.0f} ns")
+    per = [ev[(3, t + 1)] - ev[(3, t)] for t in range(2, steps - 3) if (3, t + 1) in ev and (3, t) in ev]
+    print(f"block {block}: {steps} steps, span {(max(ev.values()) - t0) / 1e3:.1f} us, "
+          f"step period median {statistics.median(per):.0f} ns")
     for w in (0, 1):
-        base = 10 + 10 * w
-        print(f"wg{w}: S ready->exp done {gap(base, base + 1):.0f} ns | exp done->dP ready "
-              f"{gap(base + 1, base + 2):.0f} | dP ready->P/dS written {gap(base + 2, base + 3):.0f} | "
-              f"P/dS written(t-1)->S ready(t) {gap(base + 3, base, -1):.0f}")
-    print(f"mma: S-slot free->Q/dO landed {gap(1, 2):.0f} ns | Q/dO landed(t)->P ready(t) {gap(2, 3):.0f} ns")
-    for t in range(2, min(steps, 6)):
-        row = [f"{e}:{(ev[(e, t)] - t0) / 1e3:.2f}" for e in (1, 2, 3, 10, 11, 12, 13, 20, 21, 22, 23) if (e, t) in ev]
+        print(f"wg{w}: S ready->exp done {gap(10, 11):.0f} | exp->dP ready {gap(11, 12):.0f} | "
+              f"dP ready->P/dS written {gap(12, 13):.0f} | written(t-1)->S ready(t) {gap(13, 10, -1):.0f} ns")
+    print(f"mma: s_free->Q landed {gap(1, 2):.0f} | Q landed->P ready {gap(2, 3):.0f} | "
+          f"P ready->dO(t+1) landed {gap(3, 4):.0f} ns")
+    for t in range(3, min(steps, 6)):
+        row = [f"{e}:{(ev[(e, t)] - t0) / 1e3:.2f}" for e in (30, 31, 1, 2, 3, 4, 10, 11, 12, 13) if (e, t) in ev]
         print(f"  t={t} " + " ".join(row))
 
 
