@@ -196,9 +196,11 @@ MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst,
                                                     void* cuda_stream);
 
 /* ---- diagnostics ------------------------------------------------------- */
-/* Event log of one backward CTA (block index `block`) into a device int64
- * buffer: [0] record count, then {event, step, globaltimer ns} triples.
- * NULL switches tracing off. Diagnostics only (tools/trace_bwd.py). */
+/* Event log of one forward / backward CTA (block index `block`) into a device
+ * int64 buffer of 1 + 5 * 2 * 8000 entries: per warp role (MMA, two
+ * elementwise warpgroups, TMA, load observer) 8000 {event << 32 | step,
+ * globaltimer ns} pairs. NULL switches tracing off. Diagnostics only
+ * (tools/trace_*.py). */
 MAGIPLAN_API magiplan_status magiplan_debug_set_trace(void* device_buffer, int32_t block);
 /* JSON-RPC access to individual planner functions for parity tests:
  * {"op": "slice_area" | "slice_area_in_cols" | "clip_slice" | "mask" |

@@ -35,6 +35,7 @@ cudaError_t launch_range_scatter_add_f32(const float* src, float* dst, const int
                                          cudaStream_t stream);
 cudaError_t launch_cast_f32_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
 void set_bwd_trace(long long* buffer, int block);
+void set_fwd_trace(long long* buffer, int block);
 }  // namespace magi
 
 struct magiplan_ffa_plan {
@@ -266,6 +267,7 @@ magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
 
 magiplan_status magiplan_debug_set_trace(void* device_buffer, int32_t block) {
   magi::set_bwd_trace(static_cast<long long*>(device_buffer), block);
+  magi::set_fwd_trace(static_cast<long long*>(device_buffer), block);
   return MAGIPLAN_OK;
 }
 

@@ -75,19 +75,6 @@ struct BwdParams {
 long long* g_trace = nullptr;
 int g_trace_block = 0;
 
-// Event log record {event, step, %globaltimer ns} of the traced CTA.
-__device__ __forceinline__ void trace_event(long long* tr, int ev, int t) {
-  if (tr == nullptr) return;
-  unsigned long long ns;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-  const unsigned long long i = atomicAdd(reinterpret_cast<unsigned long long*>(tr), 1ull);
-  if (i < 20000) {
-    tr[1 + 3 * i] = ev;
-    tr[2 + 3 * i] = t;
-    tr[3 + 3 * i] = static_cast<long long>(ns);
-  }
-}
-
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
                                           int c, float scale, bool f32, bool accumulate) {
   if (f32) {
@@ -141,16 +128,27 @@ __device__ __forceinline__ void epilogue_rows(uint32_t t_acc, bool has_work, boo
   }
 }
 
-// D[tmem] (M=128, N=128) = A[128 rows, D] . B[128 rows, D]^T, both K-major.
+// D[tmem] (M=128, N=128) = A[128 rows, D] . B[128 rows, D]^T, both K-major
+// SW128 tiles given by their descriptors; converged warp, one lane issues.
 template <int D>
-__device__ __forceinline__ void mma_rows_x_rows(uint32_t d_tmem, uint32_t a_addr, uint32_t b_addr) {
+__device__ __forceinline__ void mma_rows_x_rows(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc) {
   constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+  if constexpr (D == 128) {
+    umma_gemm_ss_k128(d_tmem, a_desc, b_desc, idesc, 0);
+  } else {
 #pragma unroll
-  for (int k = 0; k < D / 16; ++k) {
-    const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-    umma_bf16_ss(d_tmem, make_smem_desc(a_addr + off, 16, 1024), make_smem_desc(b_addr + off, 16, 1024),
-                 idesc, k > 0);
+    for (int k = 0; k < D / 16; ++k) {
+      const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+      umma_ss_elect(d_tmem, desc_add(a_desc, off), desc_add(b_desc, off), idesc, k > 0);
+    }
   }
+}
+
+// K-major SW128 descriptor (row tiles loaded by TMA) / MN-major view of the
+// same tile (16 rows per k-step, 64-column boxes kBox apart)
+__device__ __forceinline__ uint64_t kmajor_desc(const void* tile) { return make_smem_desc(smem_u32(tile), 16, 1024); }
+__device__ __forceinline__ uint64_t mnmajor_desc(const void* tile) {
+  return make_smem_desc(smem_u32(tile), kBox, 1024);
 }
 
 // 64 packed bf16-pair registers holding 128 values -> 16 x 16B swizzled smem chunks of one row.
@@ -289,16 +287,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0 && steps > 0) {
+    // converged warp; one elected lane issues every MMA / commit
+    if (steps > 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
       constexpr uint32_t idesc_q = make_idesc_bf16(128, D, false, true);
+      constexpr uint32_t kStageDesc = L::kTile >> 4;
+      const uint64_t k_desc0 = kmajor_desc(sK), v_desc0 = kmajor_desc(sV), k_mn0 = mnmajor_desc(sK);
       // A = Q / dO from TMEM (k-step = 16 head-dim elements = 8 packed columns),
       // B = K / V tile [keys, D] K-major from smem
-      auto issue_rows = [&](uint32_t d_tmem, uint32_t a_tmem, uint32_t b_addr) {
+      auto issue_rows = [&](uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc) {
+        if constexpr (D == 128) {
+          umma_gemm_ts_bk_k128(d_tmem, a_tmem, b_desc, idesc_s, 0);
+        } else {
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k) {
-          umma_bf16_ts(d_tmem, a_tmem + k * 8,
-                       make_smem_desc(b_addr + (k / 4) * kBox + (k % 4) * 32, 16, 1024), idesc_s, k > 0);
+          for (int k = 0; k < D / 16; ++k)
+            umma_ts_elect(d_tmem, a_tmem + k * 8, desc_add(b_desc, (k / 4) * kBox + (k % 4) * 32), idesc_s, k > 0);
         }
       };
       mbar_wait(&bars.qdo_full, 0);
@@ -306,11 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_wait(&bars.k_full[nst.index], nst.phase);
       mbar_wait(&bars.v_full[nst.index], nst.phase);
       tc_fence_after();
-      issue_rows(t_s, t_q, smem_u32(sK + nst.index * L::kTile));
-      umma_commit(&bars.s_full);
-      issue_rows(t_dp, t_do, smem_u32(sV + nst.index * L::kTile));
-      umma_commit(&bars.dp_full);
-      umma_commit(&bars.v_empty[nst.index]);
+      issue_rows(t_s, t_q, k_desc0 + nst.index * kStageDesc);
+      umma_commit_elect(&bars.s_full);
+      issue_rows(t_dp, t_do, v_desc0 + nst.index * kStageDesc);
+      umma_commit_elect(&bars.dp_full);
+      umma_commit_elect(&bars.v_empty[nst.index]);
       nst.advance<S>();
       for (int t = 0; t < steps; ++t) {
         const bool more = t + 1 < steps;
@@ -319,30 +322,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(&bars.k_full[nst.index], nst.phase);
           mbar_wait(&bars.v_full[nst.index], nst.phase);
           tc_fence_after();
-          issue_rows(t_s, t_q, smem_u32(sK + nst.index * L::kTile));
-          umma_commit(&bars.s_full);
+          issue_rows(t_s, t_q, k_desc0 + nst.index * kStageDesc);
+          umma_commit_elect(&bars.s_full);
         }
         mbar_wait(&bars.p_full, t & 1);
         tc_fence_after();
-        const uint32_t k_addr = smem_u32(sK + gst.index * L::kTile);
-#pragma unroll
-        for (int k = 0; k < (p.experiment == 2 ? 0 : kBlockN / 16); ++k) {
-          // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys [0,64)
-          // at +0, keys [64,128) at +64), B = K [keys, D] MN-major
-          umma_bf16_ts(t_dq, t_dp + k * 8 + (k >= 4 ? 32 : 0),
-                       make_smem_desc(k_addr + k * 16 * 128, kBox, 1024), idesc_q,
-                       (t > 0 || k > 0) ? 1u : 0u);
-        }
-        umma_commit(&bars.k_empty[gst.index]);
+        // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys [0,64)
+        // at +0, keys [64,128) at +64), B = K [keys, D] MN-major
+        if (p.experiment != 2) umma_gemm_ts_dq_k128(t_dq, t_dp, k_mn0 + gst.index * kStageDesc, idesc_q, t > 0 ? 1u : 0u);
+        umma_commit_elect(&bars.k_empty[gst.index]);
         gst.advance<S>();
         if (more) {
           // dP(t+1) overwrites the dS columns read above: in-order pipe
-          issue_rows(t_dp, t_do, smem_u32(sV + nst.index * L::kTile));
-          umma_commit(&bars.dp_full);
-          umma_commit(&bars.v_empty[nst.index]);
+          issue_rows(t_dp, t_do, v_desc0 + nst.index * kStageDesc);
+          umma_commit_elect(&bars.dp_full);
+          umma_commit_elect(&bars.v_empty[nst.index]);
           nst.advance<S>();
         } else {
-          umma_commit(&bars.done);
+          umma_commit_elect(&bars.done);
         }
       }
     }
@@ -540,7 +537,7 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
 
 namespace magi {
 // Diagnostics: route one backward CTA's event log to a device buffer
-// (int64: [0] = record count, then {event, step, ns} triples); nullptr = off.
+// (int64: [0] unused, then per-role {event << 32 | step, ns} regions); nullptr = off.
 void set_bwd_trace(long long* buffer, int block) {
   g_trace = buffer;
   g_trace_block = block;

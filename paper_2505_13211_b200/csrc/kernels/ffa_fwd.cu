@@ -7,12 +7,14 @@
 // reference proj/include/magiplan/mask.hpp:85): no atomics.
 //
 // Warp roles (320 threads):
-//   warps 0-3 / 4-7  softmax of sub-tile 0 / 1: thread = query row = TMEM
-//                    lane. Reads S (tcgen05.ld), applies the slice row bounds,
-//                    online softmax with a lazily moved max (rescale O only
-//                    when the row max grows by > 2^8), exp2 split between MUFU
-//                    and an FMA-pipe polynomial, writes P back into the S
-//                    columns as packed bf16 (tcgen05.st).
+//   warps 0-3 / 4-7  softmax, score columns [0,64) / [64,128) of BOTH
+//                    sub-tiles (thread = query row = TMEM lane): the two
+//                    warpgroups process one sub-tile together, exchange their
+//                    partial row maxima through shared memory, apply the slice
+//                    row bounds, run the online softmax with a lazily moved max
+//                    (rescale O only when the row max grows by > 2^8), exp2
+//                    split between MUFU and an FFMA2 polynomial, and write P
+//                    back into the S columns as packed bf16 (tcgen05.st).
 //   warp 8           TMA producer: Q once, K/V through a 2-stage ring.
 //   warp 9           MMA issuer (one lane). Per key tile t:
 //                      S0 = Q0 K^T, S1 = Q1 K^T           (SS, M=128 N=128)
@@ -26,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "ffa_common.cuh"
 #include "sm100.cuh"
@@ -37,8 +40,14 @@ namespace {
 constexpr int kStages = 2;
 constexpr uint32_t kBox = 128 * 64 * 2;  // one TMA box: 128 rows x 64 bf16 (128B swizzle)
 constexpr int kSub = 128;                // rows per sub-tile
-constexpr int kTileRows = 2 * kSub;
-constexpr int kThreads = 320;
+// 4 softmax warpgroups + 1 control warpgroup (TMA warp, MMA warp, 2 idle).
+// setmaxnreg split of the 96 registers per thread granted at launch: per SM
+// sub-partition 4 softmax warps x 104 + 1 control warp x 56 <= 5 x 96.
+constexpr int kThreads = 640;
+constexpr int kTmaWarp = 16;
+constexpr int kMmaWarp = 17;
+constexpr uint32_t kSoftmaxRegs = 104;
+constexpr uint32_t kControlRegs = 56;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 256 between rescales
@@ -54,7 +63,12 @@ struct FwdParams {
   float* lse;
   int32_t out_f32;
   int32_t accumulate;
+  long long* trace;  // diagnostics: per-role event log of one CTA (nullptr = off)
+  int32_t trace_block;
 };
+
+long long* g_fwd_trace = nullptr;
+int g_fwd_trace_block = 0;
 
 template <int D>
 struct FwdSmem {
@@ -62,7 +76,10 @@ struct FwdSmem {
   static constexpr uint32_t kQ = 0;  // 2 sub-tiles
   static constexpr uint32_t kK = kQ + 2 * kTileBytes;
   static constexpr uint32_t kV = kK + kStages * kTileBytes;
-  static constexpr uint32_t kBytes = kV + kStages * kTileBytes;
+  // row-max exchange [2 step parities][2 sub][2 halves][128] f32, then the
+  // row-sum exchange [2 sub][2 halves][128]
+  static constexpr uint32_t kXch = kV + kStages * kTileBytes;
+  static constexpr uint32_t kBytes = kXch + 6 * 2 * kSub * 4;
 };
 
 struct FwdBarriers {
@@ -72,34 +89,33 @@ struct FwdBarriers {
   uint64_t s_full[2], p_full[2], o_final[2];
 };
 
+// S = Q K^T (SS, both K-major): descriptors of the two tiles' first k-step;
+// a k-step is 32 B inside a 64-column box, boxes are kBox apart.
 template <int D>
-__device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint32_t q_addr, uint32_t k_addr) {
+__device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint64_t q_desc, uint64_t k_desc) {
   constexpr uint32_t idesc = make_idesc_bf16(128, 128, false, false);
+  if constexpr (D == 128) {
+    umma_gemm_ss_k128(tmem_s, q_desc, k_desc, idesc, 0);
+  } else {
 #pragma unroll
-  for (int k = 0; k < D / 16; ++k) {
-    const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
-    umma_bf16_ss(tmem_s, make_smem_desc(q_addr + off, 16, 1024), make_smem_desc(k_addr + off, 16, 1024),
-                 idesc, k > 0);
+    for (int k = 0; k < D / 16; ++k) {
+      const uint32_t off = (k / 4) * kBox + (k % 4) * 32;
+      umma_ss_elect(tmem_s, desc_add(q_desc, off), desc_add(k_desc, off), idesc, k > 0);
+    }
   }
 }
 
+// O += P V (TS): P packed bf16 in TMEM (8 columns per 16 keys), V [keys, D]
+// MN-major: a k-step is 16 key rows (2 KB).
 template <int D>
-__device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint32_t v_addr,
-                                         bool accumulate) {
+__device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint64_t v_desc, bool accumulate) {
   constexpr uint32_t idesc = make_idesc_bf16(128, D, false, true);
-#pragma unroll
-  for (int k = 0; k < kBlockN / 16; ++k) {
-    umma_bf16_ts(tmem_o, tmem_p + k * 8, make_smem_desc(v_addr + k * 16 * 128, kBox, 1024), idesc,
-                 (accumulate || k > 0) ? 1u : 0u);
-  }
+  umma_gemm_ts_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
 }
 
-__device__ __forceinline__ void tmem_st16x2(uint32_t taddr, const uint32_t* v) {
-  // 32 consecutive columns from 32 registers
-  tmem_st32(taddr, *reinterpret_cast<const uint32_t(*)[32]>(v));
-}
-
-template <int D>
+// V: softmax variant (diagnostics, MAGI_FWD_VARIANT): exp2 pairs on the FMA
+// pipe out of every 8 — 0: 2 (25%), 1: 3 (37.5%), 2: 1 (12.5%).
+template <int D, int V>
 __global__ void __launch_bounds__(kThreads, 1)
     ffa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k,
@@ -119,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int head_k = head / (p.hq / p.hk);
   const FwdTile tile = p.tiles[tile_rank];
   const int n_total = tile.n_ktiles;
+  long long* const trace = static_cast<int>(blockIdx.x) == p.trace_block ? p.trace : nullptr;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.q_full, 1);
@@ -130,12 +147,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.s_full[i], 1);
-      mbar_init(&bars.p_full[i], kSub);
+      mbar_init(&bars.p_full[i], 2 * kSub);
       mbar_init(&bars.o_final[i], 1);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc<512>(&tmem_base_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(&tmem_base_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -145,9 +162,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
 
-  if (warp == 8) {
+  if (warp >= kTmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kControlRegs));
+  if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_total > 0) {
+      Tracer tr;
+      tr.init(trace, 3);
+      int tt = 0;
       tma_prefetch_desc(&tmap_q);
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
@@ -162,11 +183,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int j = 0; j < item.n_ktiles; ++j) {
           const int k0 = item.k_begin + j * kBlockN;
           mbar_wait(&bars.k_empty[st.index], st.phase ^ 1);
+          tr.ev(30, tt);
           mbar_arrive_expect_tx(&bars.k_full[st.index], L::kTileBytes);
           for (int c = 0; c < D / 64; ++c)
             tma_load_3d(sK + st.index * L::kTileBytes + c * kBox, &tmap_k, &bars.k_full[st.index],
                         c * 64, head_k, k0);
           mbar_wait(&bars.v_empty[st.index], st.phase ^ 1);
+          tr.ev(31, tt++);
           mbar_arrive_expect_tx(&bars.v_full[st.index], L::kTileBytes);
           for (int c = 0; c < D / 64; ++c)
             tma_load_3d(sV + st.index * L::kTileBytes + c * kBox, &tmap_v, &bars.v_full[st.index],
@@ -175,169 +198,244 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == kMmaWarp + 1) {
+    // diagnostics only: observe when K / V tiles land (traced CTA)
+    if (lane == 0 && trace != nullptr && n_total > 0) {
+      Tracer tr;
+      tr.init(trace, 4);
+      PipeState st;
+      for (int t = 0; t < n_total; ++t) {
+        mbar_wait(&bars.k_full[st.index], st.phase);
+        tr.ev(32, t);
+        mbar_wait(&bars.v_full[st.index], st.phase);
+        tr.ev(33, t);
+        st.advance<kStages>();
+      }
+    }
+  } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && n_total > 0) {
-      const uint32_t q_addr0 = smem_u32(sQ), q_addr1 = smem_u32(sQ + L::kTileBytes);
+    // the whole warp runs this loop (converged); one elected lane issues
+    if (n_total > 0) {
+      const uint64_t q_desc0 = make_smem_desc(smem_u32(sQ), 16, 1024);
+      const uint64_t q_desc1 = make_smem_desc(smem_u32(sQ + L::kTileBytes), 16, 1024);
+      const uint64_t k_desc0 = make_smem_desc(smem_u32(sK), 16, 1024);
+      const uint64_t v_desc0 = make_smem_desc(smem_u32(sV), kBox, 1024);
+      constexpr uint32_t kStageDesc = L::kTileBytes >> 4;  // stage stride in descriptor units
+      Tracer tr;
+      if (lane == 0) tr.init(trace, 0);
+      tr.clk(98);
       mbar_wait(&bars.q_full, 0);
       PipeState kst, vst;
       mbar_wait(&bars.k_full[kst.index], kst.phase);
       tc_fence_after();
       {
-        const uint32_t k_addr = smem_u32(sK + kst.index * L::kTileBytes);
-        issue_qk<D>(tmem + 0, q_addr0, k_addr);
-        umma_commit(&bars.s_full[0]);
-        issue_qk<D>(tmem + 128, q_addr1, k_addr);
-        umma_commit(&bars.s_full[1]);
-        umma_commit(&bars.k_empty[kst.index]);
+        const uint64_t k_desc = k_desc0 + kst.index * kStageDesc;
+        issue_qk<D>(tmem + 0, q_desc0, k_desc);
+        umma_commit_elect(&bars.s_full[0]);
+        issue_qk<D>(tmem + 128, q_desc1, k_desc);
+        umma_commit_elect(&bars.s_full[1]);
+        umma_commit_elect(&bars.k_empty[kst.index]);
         kst.advance<kStages>();
       }
       for (int t = 0; t < n_total; ++t) {
         const bool more = t + 1 < n_total;
-        const uint32_t v_addr = smem_u32(sV + vst.index * L::kTileBytes);
+        const uint64_t v_desc = v_desc0 + vst.index * kStageDesc;
         // sub-tile 0: O0 += P0 V, then S0 for the next key tile
         mbar_wait(&bars.p_full[0], t & 1);
+        tr.ev(1, t);
         mbar_wait(&bars.v_full[vst.index], vst.phase);
+        tr.ev(2, t);
         tc_fence_after();
-        issue_pv<D>(tmem + 256, tmem + 0, v_addr, t > 0);
-        if (!more) umma_commit(&bars.o_final[0]);
-        uint32_t k_addr = 0;
+        issue_pv<D>(tmem + 256, tmem + 0, v_desc, t > 0);
+        if (!more) umma_commit_elect(&bars.o_final[0]);
+        const uint64_t k_desc = k_desc0 + kst.index * kStageDesc;
         if (more) {
           mbar_wait(&bars.k_full[kst.index], kst.phase);
+          tr.ev(3, t);
           tc_fence_after();
-          k_addr = smem_u32(sK + kst.index * L::kTileBytes);
-          issue_qk<D>(tmem + 0, q_addr0, k_addr);
-          umma_commit(&bars.s_full[0]);
+          issue_qk<D>(tmem + 0, q_desc0, k_desc);
+          umma_commit_elect(&bars.s_full[0]);
         }
         // sub-tile 1
         mbar_wait(&bars.p_full[1], t & 1);
+        tr.ev(4, t);
         tc_fence_after();
-        issue_pv<D>(tmem + 384, tmem + 128, v_addr, t > 0);
-        umma_commit(&bars.v_empty[vst.index]);
+        issue_pv<D>(tmem + 384, tmem + 128, v_desc, t > 0);
+        umma_commit_elect(&bars.v_empty[vst.index]);
         vst.advance<kStages>();
-        if (!more) umma_commit(&bars.o_final[1]);
+        if (!more) umma_commit_elect(&bars.o_final[1]);
         if (more) {
-          issue_qk<D>(tmem + 128, q_addr1, k_addr);
-          umma_commit(&bars.s_full[1]);
-          umma_commit(&bars.k_empty[kst.index]);
+          issue_qk<D>(tmem + 128, q_desc1, k_desc);
+          umma_commit_elect(&bars.s_full[1]);
+          umma_commit_elect(&bars.k_empty[kst.index]);
           kst.advance<kStages>();
         }
       }
+      tr.clk(99);
     }
-  } else {
+  } else if (warp < kTmaWarp) {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
     // ------------------------------------------------------------ softmax
-    const int sub = warp / 4;
+    // Warps 0-7 serve sub-tile 0, warps 8-15 sub-tile 1. Inside a sub-tile,
+    // warpgroup half h owns score columns [64 h, 64 h + 64) (thread = query
+    // row = TMEM lane): two warps per SM sub-partition share every sub-tile
+    // phase and the two sub-tiles' phases overlap, which keeps the MUFU pipe
+    // busy while the other sub-tile's matmuls run. The halves exchange their
+    // partial row maxima through shared memory so they agree bit for bit on
+    // the exponent base.
+    const int sub = warp / 8;
+    const int half = (warp / 4) & 1;
     const int row = (warp % 4) * 32 + lane;
-    const int q = tile.q0 + sub * kSub + row;
+    const int c0 = half * 64;       // score (key) columns of this half
+    const int oc0 = half * (D / 2);  // output columns of this half (O rescale, epilogue)
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const uint32_t t_s = tmem + sub * 128 + lane_off;
     const uint32_t t_o = tmem + 256 + sub * 128 + lane_off;
+    const uint32_t bar_id = 1 + sub;
     const float sl2 = p.scale_log2;
+    const uint32_t xch_base = smem_u32(smem + L::kXch);
     float m = -INFINITY;  // exponent base, log2 domain (lazily moved)
-    float l = 0.f;        // sum of 2^(x - m)
+    float l = 0.f;        // this half's sum of 2^(x - m)
+    const int q = tile.q0 + sub * kSub + row;
+    Tracer tr;
+    if (half == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub);
     int t = 0;
     for (int it = tile.item_begin; it < tile.item_end; ++it) {
       const FwdItem item = p.items[it];
       int32_t lo, hi;
       row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q, lo, hi);
       for (int j = 0; j < item.n_ktiles; ++j, ++t) {
-        const int k0 = item.k_begin + j * kBlockN;
+        const int kc = item.k_begin + j * kBlockN + c0;
         mbar_wait(&bars.s_full[sub], t & 1);
+        tr.ev(10, t);
         tc_fence_after();
-        uint32_t s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t(&chunk)[32] = *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]);
-          tmem_ld32(t_s + c * 32, chunk);
-        }
+        uint32_t s[64];
+        tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+        tmem_ld32(t_s + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
         tmem_ld_wait();
-
-        const bool full = lo <= k0 && k0 + kBlockN <= hi;
-        float mt = -INFINITY;
-        if (full) {
+        const bool full = lo <= kc && kc + 64 <= hi;
+        if (!full) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i) mt = fmaxf(mt, __uint_as_float(s[i]));
-        } else {
-#pragma unroll
-          for (int i = 0; i < 128; ++i) {
-            const int c = k0 + i;
-            const float v = (c >= lo && c < hi) ? __uint_as_float(s[i]) : -INFINITY;
-            s[i] = __float_as_uint(v);
-            mt = fmaxf(mt, v);
+          for (int i = 0; i < 64; ++i) {
+            const int c = kc + i;
+            if (c < lo || c >= hi) s[i] = __float_as_uint(-INFINITY);
           }
         }
+        // partial row max as 4 independent 3-input-max chains
+        float mx[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) mx[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
+#pragma unroll
+        for (int i = 8; i < 64; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
+        }
+        const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        // slot [t parity][sub][half][row]: a half can run one step ahead of the
+        // other's read, never two
+        const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 2) * kSub + row) * 4;
+        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + half * kSub * 4), "f"(pm) : "memory");
+        // both halves loaded S (P may now overwrite it) and published their max
+        named_bar_sync(bar_id, 256);
+        float po;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + (half ^ 1) * kSub * 4) : "memory");
+        const float mt = fmaxf(pm, po);
+        tr.ev(11, t);
         const float mt2 = mt * sl2;
         const bool move = mt2 > m + kRescaleThreshold;  // also true on the first finite tile
         const float alpha = move ? fast_exp2(m - mt2) : 1.f;
         if (move) m = mt2;
         const float mb = m == -INFINITY ? 0.f : m;
-        float rs = 0.f;
-        uint32_t pk[64];
+        uint32_t pk[32];
+        float rs;
         if (full) {
+          // packed f32x2: x = s * scale - m two lanes per FFMA2, sums by FADD2
+          const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
+          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-          for (int i = 0; i < 128; i += 2) {
-            const float x0 = fmaf(__uint_as_float(s[i]), sl2, -mb);
-            const float x1 = fmaf(__uint_as_float(s[i + 1]), sl2, -mb);
-            // every 4th element on the FMA pipe: MUFU ex2 is 1/8 of FMA throughput
-            const float p0 = fast_exp2(x0);
-            const float p1 = (i % 4 == 2) ? exp2_poly(x1) : fast_exp2(x1);
-            rs += p0 + p1;
-            pk[i / 2] = pack_bf16(p0, p1);
+          for (int i = 0; i < 64; i += 2) {
+            const int jj = i / 2;
+            const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
+            // pairs (jj % 8) on the FMA pipe: V0 {3, 7}, V1 {1, 4, 7}, V2 {7}
+            constexpr uint32_t kPolyMask = V == 0 ? 0x88u : (V == 1 ? 0x92u : 0x80u);
+            float p0, p1;
+            if ((kPolyMask >> (jj % 8)) & 1u) {
+              const float2 e = exp2_poly2(x.x, x.y);
+              p0 = e.x;
+              p1 = e.y;
+            } else {
+              p0 = fast_exp2(x.x);
+              p1 = fast_exp2(x.y);
+            }
+            acc2[jj % 4] = fadd2(acc2[jj % 4], f2(p0, p1));
+            pk[jj] = pack_bf16(p0, p1);
           }
+          const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
+          rs = a2.x + a2.y;
         } else {
+          float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-          for (int i = 0; i < 128; i += 2) {
+          for (int i = 0; i < 64; i += 2) {
             const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
             const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
-            rs += p0 + p1;
+            rs4[(i / 2) % 4] += p0 + p1;
             pk[i / 2] = pack_bf16(p0, p1);
           }
+          rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         }
         l = l * alpha + rs;
-        // P (bf16 pairs) into the first 64 columns of this sub-tile's S
-        tmem_st16x2(t_s, &pk[0]);
-        tmem_st16x2(t_s + 32, &pk[32]);
+        tr.ev(12, t);
+        // P (bf16 pairs): this half's 64 columns -> S columns [32 half, 32 half + 32)
+        tmem_st32(t_s + half * 32, pk);
         if (t > 0 && __any_sync(0xffffffffu, move)) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int c = 0; c < D / 64; ++c) {
             uint32_t o[32];
-            tmem_ld32(t_o + c * 32, o);
+            tmem_ld32(t_o + oc0 + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(t_o + c * 32, o);
+            tmem_st32(t_o + oc0 + c * 32, o);
           }
         }
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.p_full[sub]);
+        tr.ev(13, t);
       }
     }
 
     // ---------------------------------------------------------- epilogue
+    float* lse_ptr = p.lse + static_cast<size_t>(head) * p.seqlen_q + q;
     const bool valid = q < p.seqlen_q;
-    const bool has = l > 0.f;
-    const float lse_cur = has ? (m * kLn2 + logf(l)) : -INFINITY;
-    const float inv_l = has ? 1.f / l : 0.f;
+    const float lse_old = (p.accumulate && valid) ? *lse_ptr : -INFINITY;
+    // full row sum: this half's + the other half's (exchange slot 2)
+    float* xl = reinterpret_cast<float*>(smem + L::kXch) + 4 * 2 * kSub + sub * 2 * kSub;
+    xl[half * kSub + row] = l;
+    named_bar_sync(bar_id, 256);
+    const float lt = l + xl[(half ^ 1) * kSub + row];
+    const bool has = lt > 0.f;
+    const float lse_cur = has ? (m * kLn2 + logf(lt)) : -INFINITY;
+    const float inv_l = has ? 1.f / lt : 0.f;
     if (n_total > 0) {
       mbar_wait(&bars.o_final[sub], 0);
       tc_fence_after();
     }
-    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D;
-    float* lse_ptr = p.lse + static_cast<size_t>(head) * p.seqlen_q + q;
+    const uint32_t t_oh = t_o + oc0;
+    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + oc0;
     if (p.accumulate) {
       // merge into (out, lse) with the log-sum-exp correction; f32 output
-      const float lse_old = valid ? *lse_ptr : -INFINITY;
       const float lse_new = has ? (lse_old > lse_cur ? lse_old + log1pf(__expf(lse_cur - lse_old))
                                                      : lse_cur + log1pf(__expf(lse_old - lse_cur)))
                                 : lse_old;
       const float w_old = has ? __expf(lse_old - lse_new) : 1.f;
       const float w_cur = has ? __expf(lse_cur - lse_new) * inv_l : 0.f;
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         uint32_t o[32];
         if (n_total > 0) {
-          tmem_ld32(t_o + c * 32, o);
+          tmem_ld32(t_oh + c * 32, o);
           tmem_ld_wait();
         }
         if (valid && has) {
@@ -353,13 +451,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (valid && has) *lse_ptr = lse_new;
+      // the other half read lse_old before the barrier above
+      if (valid && has && half == 0) *lse_ptr = lse_new;
     } else {
 #pragma unroll 1
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         uint32_t o[32];
         if (n_total > 0) {
-          tmem_ld32(t_o + c * 32, o);
+          tmem_ld32(t_oh + c * 32, o);
           tmem_ld_wait();
         }
         if (!valid) continue;
@@ -387,19 +486,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (valid) *lse_ptr = lse_cur;
+      if (valid && half == 0) *lse_ptr = lse_cur;
     }
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
 }
 
-template <int D>
+template <int D, int V>
 cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, const void* v,
                             cudaStream_t stream) {
   const CUtensorMap tq = make_tmap_thd(q, prm.seqlen_q, prm.hq, D, 128);
@@ -407,10 +506,10 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t err =
-      cudaFuncSetAttribute(ffa_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ffa_fwd_kernel<D, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   const dim3 grid(static_cast<unsigned>(prm.num_tiles) * prm.hq);
-  ffa_fwd_kernel<D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, prm);
+  ffa_fwd_kernel<D, V><<<grid, kThreads, smem, stream>>>(tq, tk, tv, prm);
   return cudaGetLastError();
 }
 
@@ -436,9 +535,29 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
   prm.lse = lse;
   prm.out_f32 = out_f32;
   prm.accumulate = accumulate;
-  if (head_dim == 128) return launch_fwd_impl<128>(prm, q, k, v, stream);
-  if (head_dim == 64) return launch_fwd_impl<64>(prm, q, k, v, stream);
+  prm.trace = g_fwd_trace;
+  prm.trace_block = g_fwd_trace_block;
+  static const int variant = [] {
+    const char* e = std::getenv("MAGI_FWD_VARIANT");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (head_dim == 128) {
+    switch (variant) {
+      case 1: return launch_fwd_impl<128, 1>(prm, q, k, v, stream);
+      case 2: return launch_fwd_impl<128, 2>(prm, q, k, v, stream);
+      default: return launch_fwd_impl<128, 0>(prm, q, k, v, stream);
+    }
+  }
+  if (head_dim == 64) return launch_fwd_impl<64, 0>(prm, q, k, v, stream);
   return cudaErrorInvalidValue;
 }
 
+}  // namespace magi
+
+namespace magi {
+// Diagnostics: route one forward CTA's per-role event log to a device buffer.
+void set_fwd_trace(long long* buffer, int block) {
+  g_fwd_trace = buffer;
+  g_fwd_trace_block = block;
+}
 }  // namespace magi

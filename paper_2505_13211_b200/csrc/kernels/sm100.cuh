@@ -194,6 +194,95 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
       : "memory");
 }
 
+// ---- converged-warp issue: every lane of the MMA warp executes these and one
+// elected lane issues, so descriptor arithmetic stays on the uniform datapath
+// (a lane-0-only branch would rebuild every descriptor in vector registers
+// and move it to uniform registers before each instruction).
+__device__ __forceinline__ void umma_ss_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// One 128 x N x 128 GEMM (8 k-steps of K = 16) in a single asm block, issued
+// by one elected lane of a converged warp. SS: A and B K-major SW128 tiles of
+// two 64-column boxes (k-step = +32 B, box = +16 KB). The descriptor offsets
+// are applied in 16-byte units inside the block.
+__device__ __forceinline__ void umma_gemm_ss_k128(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, t, e;\n .reg .b64 a, b;\n"
+      " setp.ne.b32 p, %4, 0;\n setp.eq.b32 t, %4, %4;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      " add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 1024;\n add.s64 b, %2, 1024;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 1026;\n add.s64 b, %2, 1026;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 1028;\n add.s64 b, %2, 1028;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      " add.s64 a, %1, 1030;\n add.s64 b, %2, 1030;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+      "}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// TS GEMMs of 8 k-steps (K = 128) in one asm block: per step the TMEM column
+// offset of A (packed bf16, 8 columns per 16 elements) and the B descriptor
+// offset in 16-byte units are compile-time constants of the operand layout.
+#define MAGI_TS_STEP(ao, bo, pr)                                        \
+  " add.s32 a, %1, " #ao ";\n add.s64 b, %2, " #bo ";\n"              \
+  " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, " pr ";\n"
+#define MAGI_TS_GEMM(name, a0, a1, a2, a3, a4, a5, a6, a7, b0, b1, b2, b3, b4, b5, b6, b7)       \
+  __device__ __forceinline__ void name(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,        \
+                                       uint32_t idesc, uint32_t accumulate) {                   \
+    asm volatile("{\n .reg .pred p, t, e;\n .reg .b32 a;\n .reg .b64 b;\n"                    \
+                 " setp.ne.b32 p, %4, 0;\n setp.eq.b32 t, %4, %4;\n"                          \
+                 " elect.sync _|e, 0xffffffff;\n" MAGI_TS_STEP(a0, b0, "p")                   \
+                     MAGI_TS_STEP(a1, b1, "t") MAGI_TS_STEP(a2, b2, "t") MAGI_TS_STEP(a3, b3, "t") \
+                         MAGI_TS_STEP(a4, b4, "t") MAGI_TS_STEP(a5, b5, "t")                    \
+                             MAGI_TS_STEP(a6, b6, "t") MAGI_TS_STEP(a7, b7, "t") "}" ::"r"(d_tmem), \
+                 "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)                           \
+                 : "memory");                                                                   \
+  }
+// A: consecutive k-steps (8 columns apart); B MN-major (16 rows = 2 KB per step)
+MAGI_TS_GEMM(umma_gemm_ts_k128, 0, 8, 16, 24, 32, 40, 48, 56, 0, 128, 256, 384, 512, 640, 768, 896)
+// A: consecutive k-steps; B K-major SW128 (32 B per step, second 64-column box 16 KB on)
+MAGI_TS_GEMM(umma_gemm_ts_bk_k128, 0, 8, 16, 24, 32, 40, 48, 56, 0, 2, 4, 6, 1024, 1026, 1028, 1030)
+// A: the dK/dV kernel's packed P^T (or dS^T, +16) layout: query columns
+// [16k, 16k+16) at (k/4)*64 + ((k/2)%2)*32 + (k%2)*8; B MN-major
+MAGI_TS_GEMM(umma_gemm_ts_dkdv_k128, 0, 8, 32, 40, 64, 72, 96, 104, 0, 128, 256, 384, 512, 640, 768, 896)
+// A: the dQ kernel's packed dS layout: keys [0,64) at +0, [64,128) at +64; B MN-major
+MAGI_TS_GEMM(umma_gemm_ts_dq_k128, 0, 8, 16, 24, 64, 72, 80, 88, 0, 128, 256, 384, 512, 640, 768, 896)
+#undef MAGI_TS_GEMM
+
+// descriptor of the same tile advanced by `bytes` (start address field only)
+__device__ __forceinline__ uint64_t desc_add(uint64_t desc, uint32_t bytes) {
+  return desc + static_cast<uint64_t>(bytes >> 4);
+}
+
 // Arrive on an mbarrier once all previously issued tcgen05 ops of this
 // thread have completed (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
@@ -202,6 +291,36 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
           smem_u32(bar))
       : "memory");
 }
+
+// ---------------------------------------------------------------- tracing
+// Per-role event log (diagnostics, magiplan_debug_set_trace): role r writes
+// {event << 32 | step, %globaltimer ns} pairs into its own region, no atomics.
+constexpr int kTraceCap = 8000;
+struct Tracer {
+  long long* base = nullptr;
+  int n = 0;
+  __device__ __forceinline__ void init(long long* trace, int role) {
+    base = trace ? trace + 1 + static_cast<size_t>(role) * 2 * kTraceCap : nullptr;
+  }
+  __device__ __forceinline__ void ev(int e, int t) {
+    if (base == nullptr || n >= kTraceCap) return;
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(t);
+    base[2 * n + 1] = static_cast<long long>(ns);
+    ++n;
+  }
+  // {event << 32 | low 32 bits of clock64, ns}: two of these give the SM clock
+  __device__ __forceinline__ void clk(int e) {
+    if (base == nullptr || n >= kTraceCap) return;
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    const long long c = clock64();
+    base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(c);
+    base[2 * n + 1] = static_cast<long long>(ns);
+    ++n;
+  }
+};
 
 // ---------------------------------------------------------------- math
 __device__ __forceinline__ float fast_exp2(float x) {
@@ -224,6 +343,44 @@ __device__ __forceinline__ float exp2_poly(float x) {
   // bits(y) = bits(magic) + round(x); shifting by 23 moves round(x) into the exponent
   return __int_as_float(__float_as_int(p) + (__float_as_int(y) << 23) -
                         (__float_as_int(kMagic) << 23));
+}
+
+// ---- packed f32x2 (sm_100 FFMA2 / FADD2: two fp32 lanes per instruction)
+__device__ __forceinline__ uint64_t f2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ float2 f2_split(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// exp2_poly on two values with packed arithmetic (same split and polynomial)
+__device__ __forceinline__ float2 exp2_poly2(float x0, float x1) {
+  constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23
+  const uint64_t x = f2(fmaxf(x0, -126.0f), fmaxf(x1, -126.0f));
+  const uint64_t y = fadd2(x, f2(kMagic, kMagic));
+  const uint64_t r = fadd2(y, f2(-kMagic, -kMagic));  // round(x)
+  const uint64_t f = ffma2(r, f2(-1.0f, -1.0f), x);   // x - round(x)
+  uint64_t p = ffma2(f, f2(0.054602622718538274f, 0.054602622718538274f),
+                     f2(0.24192412881028413f, 0.24192412881028413f));
+  p = ffma2(p, f, f2(0.6933164806648954f, 0.6933164806648954f));
+  p = ffma2(p, f, f2(1.0f, 1.0f));
+  const float2 pp = f2_split(p), yy = f2_split(y);
+  // bits(magic) << 23 == 0 (mod 2^32): the shift leaves exactly round(x) << 23
+  return make_float2(__int_as_float(__float_as_int(pp.x) + (__float_as_int(yy.x) << 23)),
+                     __int_as_float(__float_as_int(pp.y) + (__float_as_int(yy.y) << 23)));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {

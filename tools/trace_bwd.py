@@ -27,18 +27,24 @@ def main(block: int = 0):
     do = torch.randn(S, hq, d, device="cuda", dtype=torch.bfloat16)
     out, lse = ffa_forward(plan, q, k, v)
     ffa_backward(plan, q, k, v, out, lse, do)
-    buf = torch.zeros(1 + 4 * 2 * CAP, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(1 + 5 * 2 * CAP, dtype=torch.int64, device="cuda")
     _lib.check(_lib.lib().magiplan_debug_set_trace(buf.data_ptr(), block))
     ffa_backward(plan, q, k, v, out, lse, do)
     torch.cuda.synchronize()
     _lib.check(_lib.lib().magiplan_debug_set_trace(None, 0))
-    data = buf[1:].view(4, CAP, 2).cpu().tolist()
+    data = buf[1:].view(5, CAP, 2)[:4].cpu().tolist()
     ev = {}
     for role in range(4):
         for key, ns in data[role]:
             if ns == 0:
                 break
             ev.setdefault((key >> 32, key & 0xFFFFFFFF), ns)
+    if any(k[0] == 98 for k in ev) and any(k[0] == 99 for k in ev):
+        (c0k, n0), = [(k, v) for k, v in ev.items() if k[0] == 98]
+        (c1k, n1), = [(k, v) for k, v in ev.items() if k[0] == 99]
+        dc = (c1k[1] - c0k[1]) % (1 << 32)
+        print(f"SM clock during the traced CTA: {dc / max(n1 - n0, 1) * 1e3:.0f} MHz")
+    ev = {k: v for k, v in ev.items() if k[0] < 90}
     steps = max(t for _, t in ev) + 1
     t0 = min(ev.values())
 
