@@ -474,7 +474,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
       td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
     }
-    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
+    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kDkvThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
                                                                                    td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;

@@ -40,14 +40,21 @@ namespace {
 constexpr int kStages = 2;
 constexpr uint32_t kBox = 128 * 64 * 2;  // one TMA box: 128 rows x 64 bf16 (128B swizzle)
 constexpr int kSub = 128;                // rows per sub-tile
-// 4 softmax warpgroups + 1 control warpgroup (TMA warp, MMA warp, 2 idle).
-// setmaxnreg split of the 96 registers per thread granted at launch: per SM
-// sub-partition 4 softmax warps x 104 + 1 control warp x 56 <= 5 x 96.
-constexpr int kThreads = 640;
-constexpr int kTmaWarp = 16;
-constexpr int kMmaWarp = 17;
+// Warp layouts (template PAIR):
+//   PAIR = false, 320 threads: 2 softmax warpgroups (score-column halves),
+//     each walking both sub-tiles one after the other; warp 8 TMA, warp 9 MMA.
+//   PAIR = true, 640 threads: 4 softmax warpgroups (sub-tile x column half);
+//     control warpgroup = TMA warp 16, MMA warp 17, load observer 18, idle 19.
+//     setmaxnreg split of the 96 registers per thread granted at launch: per
+//     SM sub-partition 4 softmax warps x 104 + 1 control warp x 56 <= 5 x 96.
 constexpr uint32_t kSoftmaxRegs = 104;
 constexpr uint32_t kControlRegs = 56;
+template <bool PAIR>
+struct FwdLayout {
+  static constexpr int kThreads = PAIR ? 640 : 320;
+  static constexpr int kTmaWarp = PAIR ? 16 : 8;
+  static constexpr int kMmaWarp = kTmaWarp + 1;
+};
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 constexpr float kRescaleThreshold = 8.0f;  // log2 units: P <= 256 between rescales
@@ -113,14 +120,207 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint6
   umma_gemm_ts_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
 }
 
+
+// One softmax phase: this thread's row of one sub-tile, score columns
+// [c0, c0 + 64) of key tile t (global keys from kc), against the row's
+// running (m, l). The two column halves exchange partial maxima through the
+// shared-memory slot pair at xslot and a named barrier of 256 threads.
+template <int D, int V>
+__device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int half,
+                                              int kc, int lo, int hi, int t, uint32_t xslot,
+                                              uint32_t bar_id, float sl2, uint64_t* s_full,
+                                              uint64_t* p_full, Tracer& tr, int tkey) {
+  const int c0 = half * 64;
+  const int oc0 = half * (D / 2);
+  mbar_wait(s_full, t & 1);
+  tr.ev(10, tkey);
+  tc_fence_after();
+  uint32_t s[64];
+  tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
+  tmem_ld32(t_s + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+  tmem_ld_wait();
+  const bool full = lo <= kc && kc + 64 <= hi;
+  if (!full) {
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const int c = kc + i;
+      if (c < lo || c >= hi) s[i] = __float_as_uint(-INFINITY);
+    }
+  }
+  // partial row max as 4 independent 3-input-max chains
+  float mx[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) mx[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
+#pragma unroll
+  for (int i = 8; i < 64; i += 8) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
+  }
+  const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + half * kSub * 4), "f"(pm) : "memory");
+  // both halves loaded S (P may now overwrite it) and published their max
+  named_bar_sync(bar_id, 256);
+  float po;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + (half ^ 1) * kSub * 4) : "memory");
+  const float mt = fmaxf(pm, po);
+  tr.ev(11, tkey);
+  const float mt2 = mt * sl2;
+  const bool move = mt2 > m + kRescaleThreshold;  // also true on the first finite tile
+  const float alpha = move ? fast_exp2(m - mt2) : 1.f;
+  if (move) m = mt2;
+  const float mb = m == -INFINITY ? 0.f : m;
+  uint32_t pk[32];
+  float rs;
+  if (full) {
+    // packed f32x2: x = s * scale - m two lanes per FFMA2, sums by FADD2
+    const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
+    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      const int jj = i / 2;
+      const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
+      // pairs (jj % 8) on the FMA pipe: V0 {3, 7}, V1 {1, 4, 7}, V2 {7}
+      constexpr uint32_t kPolyMask = V == 0 ? 0x88u : (V == 1 ? 0x92u : 0x80u);
+      float p0, p1;
+      if ((kPolyMask >> (jj % 8)) & 1u) {
+        const float2 e = exp2_poly2(x.x, x.y);
+        p0 = e.x;
+        p1 = e.y;
+      } else {
+        p0 = fast_exp2(x.x);
+        p1 = fast_exp2(x.y);
+      }
+      acc2[jj % 4] = fadd2(acc2[jj % 4], f2(p0, p1));
+      pk[jj] = pack_bf16(p0, p1);
+    }
+    const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
+    rs = a2.x + a2.y;
+  } else {
+    float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < 64; i += 2) {
+      const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
+      const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
+      rs4[(i / 2) % 4] += p0 + p1;
+      pk[i / 2] = pack_bf16(p0, p1);
+    }
+    rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+  }
+  l = l * alpha + rs;
+  tr.ev(12, tkey);
+  // P (bf16 pairs): this half's 64 columns -> S columns [32 half, 32 half + 32)
+  tmem_st32(t_s + half * 32, pk);
+  if (t > 0 && __any_sync(0xffffffffu, move)) {
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t o[32];
+      tmem_ld32(t_o + oc0 + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+      tmem_st32(t_o + oc0 + c * 32, o);
+    }
+  }
+  tmem_st_wait();
+  tc_fence_before();
+  mbar_arrive(p_full);
+  tr.ev(13, tkey);
+}
+
+// Output of one sub-tile row half: normalise (or merge into an existing
+// (out, lse) pair) and store. lt = full row sum, lse_old read before any
+// half of this row stored the new lse.
+template <int D>
+__device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int q, int half, float m, float lt,
+                                              float lse_old, uint32_t t_o, bool has_work, uint64_t* o_final) {
+  const int oc0 = half * (D / 2);
+  float* lse_ptr = p.lse + static_cast<size_t>(head) * p.seqlen_q + q;
+  const bool valid = q < p.seqlen_q;
+  const bool has = lt > 0.f;
+  const float lse_cur = has ? (m * kLn2 + logf(lt)) : -INFINITY;
+  const float inv_l = has ? 1.f / lt : 0.f;
+  if (has_work) {
+    mbar_wait(o_final, 0);
+    tc_fence_after();
+  }
+  const uint32_t t_oh = t_o + oc0;
+  const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + oc0;
+  if (p.accumulate) {
+    // merge into (out, lse) with the log-sum-exp correction; f32 output
+    const float lse_new = has ? (lse_old > lse_cur ? lse_old + log1pf(__expf(lse_cur - lse_old))
+                                                   : lse_cur + log1pf(__expf(lse_old - lse_cur)))
+                              : lse_old;
+    const float w_old = has ? __expf(lse_old - lse_new) : 1.f;
+    const float w_cur = has ? __expf(lse_cur - lse_new) * inv_l : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t o[32];
+      if (has_work) {
+        tmem_ld32(t_oh + c * 32, o);
+        tmem_ld_wait();
+      }
+      if (valid && has) {
+        float* dst = reinterpret_cast<float*>(p.out) + row_off + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 a = *reinterpret_cast<float4*>(dst + i);
+          a.x = a.x * w_old + __uint_as_float(o[i + 0]) * w_cur;
+          a.y = a.y * w_old + __uint_as_float(o[i + 1]) * w_cur;
+          a.z = a.z * w_old + __uint_as_float(o[i + 2]) * w_cur;
+          a.w = a.w * w_old + __uint_as_float(o[i + 3]) * w_cur;
+          *reinterpret_cast<float4*>(dst + i) = a;
+        }
+      }
+    }
+    if (valid && has && half == 0) *lse_ptr = lse_new;
+  } else {
+#pragma unroll 1
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t o[32];
+      if (has_work) {
+        tmem_ld32(t_oh + c * 32, o);
+        tmem_ld_wait();
+      }
+      if (!valid) continue;
+      if (p.out_f32) {
+        float* dst = reinterpret_cast<float*>(p.out) + row_off + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          float4 a;
+          a.x = has ? __uint_as_float(o[i + 0]) * inv_l : 0.f;
+          a.y = has ? __uint_as_float(o[i + 1]) * inv_l : 0.f;
+          a.z = has ? __uint_as_float(o[i + 2]) * inv_l : 0.f;
+          a.w = has ? __uint_as_float(o[i + 3]) * inv_l : 0.f;
+          *reinterpret_cast<float4*>(dst + i) = a;
+        }
+      } else {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + row_off + c * 32;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) {
+          uint4 v;
+          v.x = has ? pack_bf16(__uint_as_float(o[i + 0]) * inv_l, __uint_as_float(o[i + 1]) * inv_l) : 0u;
+          v.y = has ? pack_bf16(__uint_as_float(o[i + 2]) * inv_l, __uint_as_float(o[i + 3]) * inv_l) : 0u;
+          v.z = has ? pack_bf16(__uint_as_float(o[i + 4]) * inv_l, __uint_as_float(o[i + 5]) * inv_l) : 0u;
+          v.w = has ? pack_bf16(__uint_as_float(o[i + 6]) * inv_l, __uint_as_float(o[i + 7]) * inv_l) : 0u;
+          *reinterpret_cast<uint4*>(dst + i) = v;
+        }
+      }
+    }
+    if (valid && half == 0) *lse_ptr = lse_cur;
+  }
+}
+
 // V: softmax variant (diagnostics, MAGI_FWD_VARIANT): exp2 pairs on the FMA
 // pipe out of every 8 — 0: 2 (25%), 1: 3 (37.5%), 2: 1 (12.5%).
-template <int D, int V>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int D, int V, bool PAIR>
+__global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
     ffa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k,
                    const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   using L = FwdSmem<D>;
+  constexpr int kTmaWarp = FwdLayout<PAIR>::kTmaWarp;
+  constexpr int kMmaWarp = FwdLayout<PAIR>::kMmaWarp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -162,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
 
-  if (warp >= kTmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kControlRegs));
+  if (PAIR && warp >= kTmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kControlRegs));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_total > 0) {
@@ -198,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp == kMmaWarp + 1) {
+  } else if (PAIR && warp == kMmaWarp + 1) {
     // diagnostics only: observe when K / V tiles land (traced CTA)
     if (lane == 0 && trace != nullptr && n_total > 0) {
       Tracer tr;
@@ -274,219 +474,69 @@ __global__ void __launch_bounds__(kThreads, 1)
       tr.clk(99);
     }
   } else if (warp < kTmaWarp) {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
     // ------------------------------------------------------------ softmax
-    // Warps 0-7 serve sub-tile 0, warps 8-15 sub-tile 1. Inside a sub-tile,
-    // warpgroup half h owns score columns [64 h, 64 h + 64) (thread = query
-    // row = TMEM lane): two warps per SM sub-partition share every sub-tile
-    // phase and the two sub-tiles' phases overlap, which keeps the MUFU pipe
-    // busy while the other sub-tile's matmuls run. The halves exchange their
-    // partial row maxima through shared memory so they agree bit for bit on
-    // the exponent base.
-    const int sub = warp / 8;
+    // Thread = query row = TMEM lane; warpgroup half h owns score columns
+    // [64 h, 64 h + 64) of a sub-tile, and the two halves of a sub-tile
+    // exchange partial row maxima through shared memory so they agree bit for
+    // bit on the exponent base. PAIR: sub-tile = warp / 8, the two sub-tiles'
+    // phases overlap; otherwise both warpgroups walk both sub-tiles in turn.
+    if (PAIR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+    constexpr int kSubs = PAIR ? 1 : 2;  // sub-tiles this thread serves
+    const int sub0 = PAIR ? warp / 8 : 0;
     const int half = (warp / 4) & 1;
     const int row = (warp % 4) * 32 + lane;
-    const int c0 = half * 64;       // score (key) columns of this half
-    const int oc0 = half * (D / 2);  // output columns of this half (O rescale, epilogue)
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
-    const uint32_t t_s = tmem + sub * 128 + lane_off;
-    const uint32_t t_o = tmem + 256 + sub * 128 + lane_off;
-    const uint32_t bar_id = 1 + sub;
     const float sl2 = p.scale_log2;
     const uint32_t xch_base = smem_u32(smem + L::kXch);
-    float m = -INFINITY;  // exponent base, log2 domain (lazily moved)
-    float l = 0.f;        // this half's sum of 2^(x - m)
-    const int q = tile.q0 + sub * kSub + row;
+    float m[kSubs], l[kSubs];
+    int q[kSubs];
+#pragma unroll
+    for (int u = 0; u < kSubs; ++u) {
+      m[u] = -INFINITY;  // exponent base, log2 domain (lazily moved)
+      l[u] = 0.f;        // this half's sum of 2^(x - m)
+      q[u] = tile.q0 + (sub0 + u) * kSub + row;
+    }
     Tracer tr;
-    if (half == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub);
+    if (half == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub0);
     int t = 0;
     for (int it = tile.item_begin; it < tile.item_end; ++it) {
       const FwdItem item = p.items[it];
-      int32_t lo, hi;
-      row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q, lo, hi);
+      int32_t lo[kSubs], hi[kSubs];
+#pragma unroll
+      for (int u = 0; u < kSubs; ++u) row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q[u], lo[u], hi[u]);
       for (int j = 0; j < item.n_ktiles; ++j, ++t) {
-        const int kc = item.k_begin + j * kBlockN + c0;
-        mbar_wait(&bars.s_full[sub], t & 1);
-        tr.ev(10, t);
-        tc_fence_after();
-        uint32_t s[64];
-        tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-        tmem_ld32(t_s + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
-        tmem_ld_wait();
-        const bool full = lo <= kc && kc + 64 <= hi;
-        if (!full) {
+        const int kc = item.k_begin + j * kBlockN + half * 64;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            const int c = kc + i;
-            if (c < lo || c >= hi) s[i] = __float_as_uint(-INFINITY);
-          }
+        for (int u = 0; u < kSubs; ++u) {
+          const int sub = sub0 + u;
+          // slot [t parity][sub][half][row]: a half can run one step ahead of
+          // the other's read, never two
+          const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 2) * kSub + row) * 4;
+          softmax_phase<D, V>(m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off, half,
+                              kc, lo[u], hi[u], t, xslot, PAIR ? 1 + sub : 1, sl2, &bars.s_full[sub],
+                              &bars.p_full[sub], tr, kSubs * t + u);
         }
-        // partial row max as 4 independent 3-input-max chains
-        float mx[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) mx[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
-#pragma unroll
-        for (int i = 8; i < 64; i += 8) {
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
-        }
-        const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-        // slot [t parity][sub][half][row]: a half can run one step ahead of the
-        // other's read, never two
-        const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 2) * kSub + row) * 4;
-        asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + half * kSub * 4), "f"(pm) : "memory");
-        // both halves loaded S (P may now overwrite it) and published their max
-        named_bar_sync(bar_id, 256);
-        float po;
-        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + (half ^ 1) * kSub * 4) : "memory");
-        const float mt = fmaxf(pm, po);
-        tr.ev(11, t);
-        const float mt2 = mt * sl2;
-        const bool move = mt2 > m + kRescaleThreshold;  // also true on the first finite tile
-        const float alpha = move ? fast_exp2(m - mt2) : 1.f;
-        if (move) m = mt2;
-        const float mb = m == -INFINITY ? 0.f : m;
-        uint32_t pk[32];
-        float rs;
-        if (full) {
-          // packed f32x2: x = s * scale - m two lanes per FFMA2, sums by FADD2
-          const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
-          uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-#pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            const int jj = i / 2;
-            const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
-            // pairs (jj % 8) on the FMA pipe: V0 {3, 7}, V1 {1, 4, 7}, V2 {7}
-            constexpr uint32_t kPolyMask = V == 0 ? 0x88u : (V == 1 ? 0x92u : 0x80u);
-            float p0, p1;
-            if ((kPolyMask >> (jj % 8)) & 1u) {
-              const float2 e = exp2_poly2(x.x, x.y);
-              p0 = e.x;
-              p1 = e.y;
-            } else {
-              p0 = fast_exp2(x.x);
-              p1 = fast_exp2(x.y);
-            }
-            acc2[jj % 4] = fadd2(acc2[jj % 4], f2(p0, p1));
-            pk[jj] = pack_bf16(p0, p1);
-          }
-          const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
-          rs = a2.x + a2.y;
-        } else {
-          float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-          for (int i = 0; i < 64; i += 2) {
-            const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
-            rs4[(i / 2) % 4] += p0 + p1;
-            pk[i / 2] = pack_bf16(p0, p1);
-          }
-          rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-        }
-        l = l * alpha + rs;
-        tr.ev(12, t);
-        // P (bf16 pairs): this half's 64 columns -> S columns [32 half, 32 half + 32)
-        tmem_st32(t_s + half * 32, pk);
-        if (t > 0 && __any_sync(0xffffffffu, move)) {
-#pragma unroll 1
-          for (int c = 0; c < D / 64; ++c) {
-            uint32_t o[32];
-            tmem_ld32(t_o + oc0 + c * 32, o);
-            tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st32(t_o + oc0 + c * 32, o);
-          }
-        }
-        tmem_st_wait();
-        tc_fence_before();
-        mbar_arrive(&bars.p_full[sub]);
-        tr.ev(13, t);
       }
     }
 
     // ---------------------------------------------------------- epilogue
-    float* lse_ptr = p.lse + static_cast<size_t>(head) * p.seqlen_q + q;
-    const bool valid = q < p.seqlen_q;
-    const float lse_old = (p.accumulate && valid) ? *lse_ptr : -INFINITY;
-    // full row sum: this half's + the other half's (exchange slot 2)
-    float* xl = reinterpret_cast<float*>(smem + L::kXch) + 4 * 2 * kSub + sub * 2 * kSub;
-    xl[half * kSub + row] = l;
-    named_bar_sync(bar_id, 256);
-    const float lt = l + xl[(half ^ 1) * kSub + row];
-    const bool has = lt > 0.f;
-    const float lse_cur = has ? (m * kLn2 + logf(lt)) : -INFINITY;
-    const float inv_l = has ? 1.f / lt : 0.f;
-    if (n_total > 0) {
-      mbar_wait(&bars.o_final[sub], 0);
-      tc_fence_after();
-    }
-    const uint32_t t_oh = t_o + oc0;
-    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + oc0;
-    if (p.accumulate) {
-      // merge into (out, lse) with the log-sum-exp correction; f32 output
-      const float lse_new = has ? (lse_old > lse_cur ? lse_old + log1pf(__expf(lse_cur - lse_old))
-                                                     : lse_cur + log1pf(__expf(lse_old - lse_cur)))
-                                : lse_old;
-      const float w_old = has ? __expf(lse_old - lse_new) : 1.f;
-      const float w_cur = has ? __expf(lse_cur - lse_new) * inv_l : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t o[32];
-        if (n_total > 0) {
-          tmem_ld32(t_oh + c * 32, o);
-          tmem_ld_wait();
-        }
-        if (valid && has) {
-          float* dst = reinterpret_cast<float*>(p.out) + row_off + c * 32;
+    float lse_old[kSubs];
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 a = *reinterpret_cast<float4*>(dst + i);
-            a.x = a.x * w_old + __uint_as_float(o[i + 0]) * w_cur;
-            a.y = a.y * w_old + __uint_as_float(o[i + 1]) * w_cur;
-            a.z = a.z * w_old + __uint_as_float(o[i + 2]) * w_cur;
-            a.w = a.w * w_old + __uint_as_float(o[i + 3]) * w_cur;
-            *reinterpret_cast<float4*>(dst + i) = a;
-          }
-        }
-      }
-      // the other half read lse_old before the barrier above
-      if (valid && has && half == 0) *lse_ptr = lse_new;
-    } else {
-#pragma unroll 1
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t o[32];
-        if (n_total > 0) {
-          tmem_ld32(t_oh + c * 32, o);
-          tmem_ld_wait();
-        }
-        if (!valid) continue;
-        if (p.out_f32) {
-          float* dst = reinterpret_cast<float*>(p.out) + row_off + c * 32;
+    for (int u = 0; u < kSubs; ++u)
+      lse_old[u] = (p.accumulate && q[u] < p.seqlen_q) ? p.lse[static_cast<size_t>(head) * p.seqlen_q + q[u]]
+                                                      : -INFINITY;
+    // full row sums: this half's + the other half's; the barrier also orders
+    // every half's lse_old read before any lse store
+    float* xl = reinterpret_cast<float*>(smem + L::kXch) + 4 * 2 * kSub;  // [sub][half][row]
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            float4 a;
-            a.x = has ? __uint_as_float(o[i + 0]) * inv_l : 0.f;
-            a.y = has ? __uint_as_float(o[i + 1]) * inv_l : 0.f;
-            a.z = has ? __uint_as_float(o[i + 2]) * inv_l : 0.f;
-            a.w = has ? __uint_as_float(o[i + 3]) * inv_l : 0.f;
-            *reinterpret_cast<float4*>(dst + i) = a;
-          }
-        } else {
-          __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(p.out) + row_off + c * 32;
+    for (int u = 0; u < kSubs; ++u) xl[((sub0 + u) * 2 + half) * kSub + row] = l[u];
+    named_bar_sync(PAIR ? 1 + sub0 : 1, 256);
 #pragma unroll
-          for (int i = 0; i < 32; i += 8) {
-            uint4 v;
-            v.x = has ? pack_bf16(__uint_as_float(o[i + 0]) * inv_l, __uint_as_float(o[i + 1]) * inv_l) : 0u;
-            v.y = has ? pack_bf16(__uint_as_float(o[i + 2]) * inv_l, __uint_as_float(o[i + 3]) * inv_l) : 0u;
-            v.z = has ? pack_bf16(__uint_as_float(o[i + 4]) * inv_l, __uint_as_float(o[i + 5]) * inv_l) : 0u;
-            v.w = has ? pack_bf16(__uint_as_float(o[i + 6]) * inv_l, __uint_as_float(o[i + 7]) * inv_l) : 0u;
-            *reinterpret_cast<uint4*>(dst + i) = v;
-          }
-        }
-      }
-      if (valid && half == 0) *lse_ptr = lse_cur;
+    for (int u = 0; u < kSubs; ++u) {
+      const int sub = sub0 + u;
+      const float lt = l[u] + xl[(sub * 2 + (half ^ 1)) * kSub + row];
+      softmax_store<D>(p, head, q[u], half, m[u], lt, lse_old[u], tmem + 256 + sub * 128 + lane_off, n_total > 0,
+                       &bars.o_final[sub]);
     }
   }
 
@@ -498,7 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D, int V>
+template <int D, int V, bool PAIR>
 cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, const void* v,
                             cudaStream_t stream) {
   const CUtensorMap tq = make_tmap_thd(q, prm.seqlen_q, prm.hq, D, 128);
@@ -506,10 +556,10 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t err =
-      cudaFuncSetAttribute(ffa_fwd_kernel<D, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ffa_fwd_kernel<D, V, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   const dim3 grid(static_cast<unsigned>(prm.num_tiles) * prm.hq);
-  ffa_fwd_kernel<D, V><<<grid, kThreads, smem, stream>>>(tq, tk, tv, prm);
+  ffa_fwd_kernel<D, V, PAIR><<<grid, FwdLayout<PAIR>::kThreads, smem, stream>>>(tq, tk, tv, prm);
   return cudaGetLastError();
 }
 
@@ -541,14 +591,20 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
     const char* e = std::getenv("MAGI_FWD_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
+  // default: 320-thread layout, 37.5% of the exponentials on the FMA pipe
+  // (measured best on config 2); MAGI_FWD_VARIANT selects the alternatives
+  // for A/B runs: bit 0 = 640-thread layout, bits 1-2 = polynomial share.
   if (head_dim == 128) {
     switch (variant) {
-      case 1: return launch_fwd_impl<128, 1>(prm, q, k, v, stream);
-      case 2: return launch_fwd_impl<128, 2>(prm, q, k, v, stream);
-      default: return launch_fwd_impl<128, 0>(prm, q, k, v, stream);
+      case 1: return launch_fwd_impl<128, 0, true>(prm, q, k, v, stream);
+      case 3: return launch_fwd_impl<128, 1, true>(prm, q, k, v, stream);
+      case 4: return launch_fwd_impl<128, 0, false>(prm, q, k, v, stream);
+      case 5: return launch_fwd_impl<128, 2, true>(prm, q, k, v, stream);
+      case 6: return launch_fwd_impl<128, 2, false>(prm, q, k, v, stream);
+      default: return launch_fwd_impl<128, 1, false>(prm, q, k, v, stream);
     }
   }
-  if (head_dim == 64) return launch_fwd_impl<64, 0>(prm, q, k, v, stream);
+  if (head_dim == 64) return launch_fwd_impl<64, 1, false>(prm, q, k, v, stream);
   return cudaErrorInvalidValue;
 }
 

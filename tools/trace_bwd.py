@@ -1,8 +1,8 @@
 """Timeline of one dK/dV CTA (diagnostics; see magiplan_debug_set_trace).
 
-Per-role logs (globaltimer ns): MMA 1 = S slot free, 2 = Q(t+1) landed,
-3 = P/dS(t) ready, 4 = dO(t+1) landed; warpgroups 10..13 = S(t) ready, exp
-done, dP(t) ready, P/dS(t) written; TMA 30 / 31 = Q / dO slot for step t free.
+Per-role logs (globaltimer ns): MMA 1 = P^T(t) ready, 2 = Q(t+1) landed,
+3 = dS^T(t) ready, 4 = dO(t+1) landed; warpgroups 10..13 = S(t) ready, P^T
+written, dP(t) ready, dS^T(t) written; TMA 30 / 31 = Q / dO slot for step t free.
 """
 import statistics
 import sys
@@ -56,10 +56,10 @@ def main(block: int = 0):
     print(f"block {block}: {steps} steps, span {(max(ev.values()) - t0) / 1e3:.1f} us, "
           f"step period median {statistics.median(per):.0f} ns")
     for w in (0, 1):
-        print(f"wg{w}: S ready->exp done {gap(10, 11):.0f} | exp->dP ready {gap(11, 12):.0f} | "
-              f"dP ready->P/dS written {gap(12, 13):.0f} | written(t-1)->S ready(t) {gap(13, 10, -1):.0f} ns")
-    print(f"mma: s_free->Q landed {gap(1, 2):.0f} | Q landed->P ready {gap(2, 3):.0f} | "
-          f"P ready->dO(t+1) landed {gap(3, 4):.0f} ns")
+        print(f"wg{w}: S ready->P written {gap(10, 11):.0f} | P->dP ready {gap(11, 12):.0f} | "
+              f"dP ready->dS written {gap(12, 13):.0f} | dS written(t-1)->S ready(t) {gap(13, 10, -1):.0f} ns")
+    print(f"mma: P ready->Q(t+1) landed {gap(1, 2):.0f} | Q landed->dS ready {gap(2, 3):.0f} | "
+          f"dS ready->dO(t+1) landed {gap(3, 4):.0f} ns")
     for t in range(3, min(steps, 6)):
         row = [f"{e}:{(ev[(e, t)] - t0) / 1e3:.2f}" for e in (30, 31, 1, 2, 3, 4, 10, 11, 12, 13) if (e, t) in ev]
         print(f"  t={t} " + " ".join(row))
