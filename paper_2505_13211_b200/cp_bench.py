@@ -12,17 +12,25 @@ from __future__ import annotations
 import json
 import os
 import statistics
+from pathlib import Path
 
 import torch
 import torch.distributed as dist
 
 PER_RANK = 131072
 HQ, HK, D, BLOCK = 48, 8, 128, 8192
-# B200 cost model for the overlap solver: ~800 TFLOPS FFA, ~300 GB/s effective cast
+# B200 cost model for the overlap solver: the fitted one when
+# tools/calibrate_cost_model.py has been run (configs/cost_model_b200.json),
+# else analytic figures (~800 TFLOPS FFA, ~300 GB/s effective cast).
 COST = {"ffa_fwd": {"latency": 20, "per_unit": 4 * HQ * D / 8.0e8},
         "ffa_bwd": {"latency": 20, "per_unit": 10 * HQ * D / 6.0e8},
         "cast": {"latency": 30, "per_unit": (2 * HK * D * 2) / 3.0e5},
         "reduce": {"latency": 30, "per_unit": (2 * HK * D * 4) / 3.0e5}}
+_FITTED = Path(__file__).resolve().parents[1] / "configs" / "cost_model_b200.json"
+if _FITTED.exists():
+    _fit = json.loads(_FITTED.read_text())
+    COST.update({k: {"latency": v["latency"], "per_unit": v["per_unit"]} for k, v in _fit.items()
+                 if k in COST and isinstance(v, dict)})
 
 
 def scenario(cp: int) -> dict:
