@@ -399,10 +399,20 @@ __global__ void __launch_bounds__(kThreads, 1)
               mbar_arrive(&bars.s_free);
             }
             if (all_in) {
+              // x = s * scale * log2e - lse * log2e, two lanes per FFMA2; a
+              // quarter of the exponentials on the FMA pipe
+              const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) {
-                const float x = fmaf(__uint_as_float(s[c]), sl2, -lse_l2);
-                pv[h2 * 32 + c] = (c % 4 == 3) ? exp2_poly(x) : fast_exp2(x);
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
+                if (c % 8 == 6) {
+                  const float2 e = exp2_poly2(x.x, x.y);
+                  pv[h2 * 32 + c] = e.x;
+                  pv[h2 * 32 + c + 1] = e.y;
+                } else {
+                  pv[h2 * 32 + c] = fast_exp2(x.x);
+                  pv[h2 * 32 + c + 1] = fast_exp2(x.y);
+                }
               }
             } else {
 #pragma unroll
@@ -421,11 +431,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           uint32_t dp[32], ds[16];
           tmem_ld32(t_dp + lane_off + col0 + c * 32, dp);
           tmem_ld_wait();
+          const uint64_t nd2 = f2(-dlt, -dlt);
 #pragma unroll
           for (int j2 = 0; j2 < 32; j2 += 2) {
             const int col = c * 32 + j2;
-            ds[j2 / 2] = pack_bf16(pv[col] * (__uint_as_float(dp[j2]) - dlt),
-                                   pv[col + 1] * (__uint_as_float(dp[j2 + 1]) - dlt));
+            // dS = P (dP - delta): FADD2 + FMUL2 per pair
+            const float2 d = f2_split(fmul2(f2(pv[col], pv[col + 1]),
+                                            fadd2(f2(__uint_as_float(dp[j2]), __uint_as_float(dp[j2 + 1])), nd2)));
+            ds[j2 / 2] = pack_bf16(d.x, d.y);
           }
           // dS chunk -> this warpgroup's consumed dP columns [col0 + c*16, +16)
           tmem_st16(t_dp + lane_off + col0 + c * 16, ds);
@@ -464,7 +477,14 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   cudaError_t err = cudaSuccess;
   if ((parts & 1) && num_k_tiles > 0) {
     const int smem = DkvSmem<D>::kBytes;  // 1024-aligned dynamic window, barriers inside
-    err = cudaFuncSetAttribute(ffa_bwd_dkdv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static const int poly = [] {
+      const char* e = std::getenv("MAGI_BWD_POLY");
+      return e ? std::atoi(e) : 0;
+    }();
+    // default 37.5% of the exponentials on the FMA pipe (measured best)
+    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0>
+                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2> : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3> : ffa_bwd_dkdv_kernel<D, 1>));
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
     BwdParams pk = prm;
@@ -474,7 +494,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
       td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
     }
-    ffa_bwd_dkdv_kernel<D><<<dim3(num_k_tiles * prm.hk), kDkvThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
+    kern<<<dim3(num_k_tiles * prm.hk), kDkvThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
                                                                                    td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
