@@ -426,6 +426,8 @@ def main() -> None:
     ap.add_argument("--impl", default="magi", choices=["magi", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cp-mode", default="magi", choices=["magi", "ring"],
+                    help="N>1 only: MagiAttention GroupCast CP (default) or the ring-attention baseline")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -51,7 +51,13 @@ def run(args) -> None:
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    cpa = CPAttention(scenario(world), HQ, HK, D)
+    ring = getattr(args, "cp_mode", "magi") == "ring"
+    if ring:
+        from paper_2505_13211_b200.ring import RingAttention
+
+        cpa = RingAttention(scenario(world)["workload"]["mask"], HQ, HK, D)
+    else:
+        cpa = CPAttention(scenario(world), HQ, HK, D)
     L = cpa.local_tokens
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     q_h = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).pin_memory()
@@ -117,20 +123,27 @@ def run(args) -> None:
         value = total / (ms.item() * 1e-3) / 1e12
         per_gpu = value / world
         n_launch = 0
-        for st in cpa.fwd_stages:
-            n_launch += 1 + 2 * (1 if sum(st.send_splits) else 0)
-        for st in cpa.bwd_stages:
-            n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
-        n_launch += 2 + 1 + 2 + 3  # host fwd + cast, preprocess, host bwd (2), final casts
+        if ring:
+            n_plans = sum(p is not None for p in cpa.plans)
+            n_launch = n_plans * 3 + 1 + 1 + 3  # fwd + dq + dkdv per plan, cast, preprocess, final casts
+        else:
+            for st in cpa.fwd_stages:
+                n_launch += 1 + 2 * (1 if sum(st.send_splits) else 0)
+            for st in cpa.bwd_stages:
+                n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
+            n_launch += 2 + 1 + 2 + 3  # host fwd + cast, preprocess, host bwd (2), final casts
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms.item(), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "cp_block_causal_magi1_24b", "seqlen": PER_RANK * world,
                        "tokens_per_rank": PER_RANK, "num_heads_q": HQ, "num_heads_k": HK, "head_dim": D,
-                       "mask": f"block_causal(block={BLOCK})", "dispatch": "greedy",
-                       "dispatch_chunk_size": cpa.chunk_size, "num_stages_fwd": cpa.xplan["num_stages_fwd"],
-                       "num_stages_bwd": cpa.xplan["num_stages_bwd"], "parallelism": f"cp{world}",
+                       "mask": f"block_causal(block={BLOCK})", "dispatch": "zigzag" if ring else "greedy",
+                       "cp_mode": "ring" if ring else "magi",
+                       "dispatch_chunk_size": cpa.chunk_size,
+                       "num_stages_fwd": world if ring else cpa.xplan["num_stages_fwd"],
+                       "num_stages_bwd": world if ring else cpa.xplan["num_stages_bwd"],
+                       "parallelism": f"cp{world}",
                        "flops_per_step": total,
                        "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),
                        "comm_tokens_all_ranks": dict(zip(cpa.comm_tokens().keys(), comm[0].tolist())),

@@ -67,6 +67,30 @@ std::string debug_eval(const std::string& request) {
     for (const auto& p : clip_slice(slice_of(r["slice"]), {r["rows"][0].get<Token>(), r["rows"][1].get<Token>()},
                                     {r["cols"][0].get<Token>(), r["cols"][1].get<Token>()}))
       out.push_back(slice_json(p));
+  } else if (op == "chunk_pair_slices") {
+    // slices of the mask between the query rows of chunk list `q_chunks` and
+    // the key columns of chunk list `k_chunks` (chunk = `chunk` tokens), in the
+    // local coordinates of buffers that hold those chunks back to back in list
+    // order: the ring-attention baseline's per-(rank, source) work
+    const AttnMask m = mask_of(r["mask"]);
+    const Token cs = r["chunk"].get<Token>();
+    const auto qc = r["q_chunks"].get<std::vector<int64_t>>();
+    const auto kc = r["k_chunks"].get<std::vector<int64_t>>();
+    out = json::array();
+    for (std::size_t i = 0; i < qc.size(); ++i) {
+      const TokenRange rows{qc[i] * cs, (qc[i] + 1) * cs};
+      for (std::size_t j = 0; j < kc.size(); ++j) {
+        const TokenRange cols{kc[j] * cs, (kc[j] + 1) * cs};
+        for (const auto& sl : m.slices) {
+          for (const auto& pc : clip_slice(sl, rows, cols)) {
+            const Token dq = static_cast<Token>(i) * cs - rows.start;
+            const Token dk = static_cast<Token>(j) * cs - cols.start;
+            out.push_back(json::array({pc.q.start + dq, pc.q.end + dq, pc.k.start + dk, pc.k.end + dk,
+                                       static_cast<int>(pc.type)}));
+          }
+        }
+      }
+    }
   } else if (op == "mask") {
     const AttnMask m = mask_of(r["mask"]);
     out["json"] = json::parse(mask_to_json(m));

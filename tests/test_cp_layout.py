@@ -136,3 +136,31 @@ def test_groupcast_groupreduce_exchange_gloo(built_lib, world):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+@pytest.mark.parametrize("mask", [
+    {"seqlen": 4096, "pattern": "causal"},
+    {"seqlen": 8192, "pattern": "block_causal", "params": {"block_size": 1024}},
+    {"seqlen": 4096, "pattern": "varlen_block_causal_last_global",
+     "params": {"sample_lengths": [2048, 1024, 1024], "block_size": 512}},
+])
+@pytest.mark.parametrize("cp", [2, 4])
+def test_ring_plan_covers_mask(built_lib, mask, cp):
+    """Ring-attention baseline work lists (zigzag chunks x source rank) cover
+    the mask's MULTIPLICITY area exactly, and stay inside the local buffers."""
+    from paper_2505_13211_b200.planner import debug_eval
+
+    S = mask["seqlen"]
+    cs = S // (2 * cp)
+    areas = debug_eval("shard", mask=mask, chunk=cs)
+    asg = debug_eval("zigzag", areas=areas, cp=cp)["assignment"]
+    chunks = [[i for i, a in enumerate(asg) if a == r] for r in range(cp)]
+    assert sorted(sum(chunks, [])) == list(range(2 * cp))
+    total = 0
+    for r in range(cp):
+        for s in range(cp):
+            sl = debug_eval("chunk_pair_slices", mask=mask, chunk=cs, q_chunks=chunks[r], k_chunks=chunks[s])
+            for qs, qe, ks, ke, _t in sl:
+                assert 0 <= qs < qe <= len(chunks[r]) * cs and 0 <= ks < ke <= len(chunks[s]) * cs
+            total += sum(debug_eval("slice_area", slice=x) for x in sl)
+    assert total == debug_eval("mask", mask=mask)["area_multiplicity"]

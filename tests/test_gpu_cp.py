@@ -15,7 +15,7 @@ COST = {"ffa_fwd": {"latency": 30, "per_unit": 8.19e-05}, "ffa_bwd": {"latency":
         "cast": {"latency": 10, "per_unit": 0.0082}, "reduce": {"latency": 10, "per_unit": 0.0082}}
 
 
-def _worker(rank, world, port, mask, chunk, hq, hk, d, outq):
+def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode="magi"):
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -23,12 +23,17 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq):
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
     try:
         from paper_2505_13211_b200.cp import CPAttention
+        from paper_2505_13211_b200.ring import RingAttention
 
-        scen = {"workload": {"mask": mask, "num_heads_q": hq, "num_heads_k": hk, "head_dim": d},
-                "cp_size": world, "dispatch_chunk_size": chunk, "cost_model": COST,
-                "overlap": {"min_chunk_size": 128, "max_num_chunks": 4}}
-        cpa = CPAttention(scen, hq, hk, d)
-        S = cpa.xplan["seqlen"]
+        if mode == "ring":
+            cpa = RingAttention(mask, hq, hk, d)
+            S = cpa.chunk_size * 2 * world
+        else:
+            scen = {"workload": {"mask": mask, "num_heads_q": hq, "num_heads_k": hk, "head_dim": d},
+                    "cp_size": world, "dispatch_chunk_size": chunk, "cost_model": COST,
+                    "overlap": {"min_chunk_size": 128, "max_num_chunks": 4}}
+            cpa = CPAttention(scen, hq, hk, d)
+            S = cpa.xplan["seqlen"]
         g = torch.Generator().manual_seed(11)
         Q = torch.randn(S, hq, d, generator=g).to(torch.bfloat16)
         K = torch.randn(S, hk, d, generator=g).to(torch.bfloat16)
@@ -47,13 +52,16 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mask,chunk", [
-    ({"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 256),
-    ({"seqlen": 2048, "pattern": "varlen_block_causal_last_global",
-      "params": {"sample_lengths": [1024, 512, 512], "block_size": 256}}, 128),
-    ({"seqlen": 3072, "pattern": "causal"}, 192),
+@pytest.mark.parametrize("mode,mask,chunk", [
+    ("magi", {"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 256),
+    ("magi", {"seqlen": 2048, "pattern": "varlen_block_causal_last_global",
+              "params": {"sample_lengths": [1024, 512, 512], "block_size": 256}}, 128),
+    ("magi", {"seqlen": 3072, "pattern": "causal"}, 192),
+    # ring-attention baseline (zigzag dispatch, K/V around the ring)
+    ("ring", {"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 0),
+    ("ring", {"seqlen": 4096, "pattern": "causal"}, 0),
 ])
-def test_cp_matches_oracle(built_lib, cuda, mask, chunk):
+def test_cp_matches_oracle(built_lib, cuda, mode, mask, chunk):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     from oracle import oracle
@@ -63,8 +71,9 @@ def test_cp_matches_oracle(built_lib, cuda, mask, chunk):
     hq, hk, d = 4, 2, 128
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
-    port = 29700 + chunk % 97
-    ps = [ctx.Process(target=_worker, args=(r, world, port, mask, chunk, hq, hk, d, qu)) for r in range(world)]
+    port = 29700 + chunk % 97 + (37 if mode == "ring" else 0) + (mask["seqlen"] % 89)
+    ps = [ctx.Process(target=_worker, args=(r, world, port, mask, chunk, hq, hk, d, qu, mode))
+          for r in range(world)]
     for p in ps:
         p.start()
     res = [qu.get(timeout=120) for _ in range(world)]
