@@ -40,19 +40,25 @@ namespace {
 constexpr int kStages = 2;
 constexpr uint32_t kBox = 128 * 64 * 2;  // one TMA box: 128 rows x 64 bf16 (128B swizzle)
 constexpr int kSub = 128;                // rows per sub-tile
-// Warp layouts (template PAIR):
-//   PAIR = false, 320 threads: 2 softmax warpgroups (score-column halves),
-//     each walking both sub-tiles one after the other; warp 8 TMA, warp 9 MMA.
-//   PAIR = true, 640 threads: 4 softmax warpgroups (sub-tile x column half);
-//     control warpgroup = TMA warp 16, MMA warp 17, load observer 18, idle 19.
-//     setmaxnreg split of the 96 registers per thread granted at launch: per
-//     SM sub-partition 4 softmax warps x 104 + 1 control warp x 56 <= 5 x 96.
+// Warp layouts (template LAYOUT). A sub-tile's 128 score columns are split
+// into NP parts, one softmax warpgroup each (thread = query row):
+//   0: 320 threads, NP = 2: two warpgroups walk both sub-tiles one after the
+//      other; warp 8 TMA, warp 9 MMA.
+//   1: 640 threads, NP = 2: four warpgroups (sub-tile x half), the two
+//      sub-tiles' phases overlap; control warpgroup = TMA warp 16, MMA warp 17,
+//      load observer 18, idle 19; setmaxnreg split of the 96 registers per
+//      thread granted at launch: per SM sub-partition 4 softmax warps x 104 +
+//      1 control warp x 56 <= 5 x 96.
+//   2: 576 threads, NP = 4: four warpgroups (32 columns each) walk both
+//      sub-tiles one after the other; warp 16 TMA, warp 17 MMA.
 constexpr uint32_t kSoftmaxRegs = 104;
 constexpr uint32_t kControlRegs = 56;
-template <bool PAIR>
+template <int LAYOUT>
 struct FwdLayout {
-  static constexpr int kThreads = PAIR ? 640 : 320;
-  static constexpr int kTmaWarp = PAIR ? 16 : 8;
+  static constexpr bool kPair = LAYOUT == 1;
+  static constexpr int kParts = LAYOUT == 2 ? 4 : 2;
+  static constexpr int kThreads = LAYOUT == 0 ? 320 : (LAYOUT == 1 ? 640 : 576);
+  static constexpr int kTmaWarp = LAYOUT == 0 ? 8 : 16;
   static constexpr int kMmaWarp = kTmaWarp + 1;
 };
 constexpr float kLog2e = 1.4426950408889634f;
@@ -83,10 +89,11 @@ struct FwdSmem {
   static constexpr uint32_t kQ = 0;  // 2 sub-tiles
   static constexpr uint32_t kK = kQ + 2 * kTileBytes;
   static constexpr uint32_t kV = kK + kStages * kTileBytes;
-  // row-max exchange [2 step parities][2 sub][2 halves][128] f32, then the
-  // row-sum exchange [2 sub][2 halves][128]
+  // row-max exchange [2 step parities][2 sub][4 parts][128] f32, then the
+  // row-sum exchange [2 sub][4 parts][128]
   static constexpr uint32_t kXch = kV + kStages * kTileBytes;
-  static constexpr uint32_t kBytes = kXch + 6 * 2 * kSub * 4;
+  static constexpr uint32_t kXl = 16 * kSub;  // float offset of the row-sum exchange
+  static constexpr uint32_t kBytes = kXch + 24 * kSub * 4;
 };
 
 struct FwdBarriers {
@@ -112,37 +119,45 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint64_t q_desc, uint6
   }
 }
 
-// O += P V (TS): P packed bf16 in TMEM (8 columns per 16 keys), V [keys, D]
-// MN-major: a k-step is 16 key rows (2 KB).
-template <int D>
+// O += P V (TS): P packed bf16 in TMEM, V [keys, D] MN-major (a k-step is
+// 16 key rows, 2 KB). Each softmax part writes its keys' P into the first
+// columns of its own S columns: NP = 2 -> keys [0,64) at +0, [64,128) at +64;
+// NP = 4 -> keys [32w, 32w+32) at +32w.
+template <int D, int NP>
 __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint64_t v_desc, bool accumulate) {
   constexpr uint32_t idesc = make_idesc_bf16(128, D, false, true);
-  umma_gemm_ts_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
+  if constexpr (NP == 2) {
+    umma_gemm_ts_dq_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
+  } else {
+    umma_gemm_ts_dkdv_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
+  }
 }
 
 
 // One softmax phase: this thread's row of one sub-tile, score columns
-// [c0, c0 + 64) of key tile t (global keys from kc), against the row's
-// running (m, l). The two column halves exchange partial maxima through the
-// shared-memory slot pair at xslot and a named barrier of 256 threads.
-template <int D, int V>
-__device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int half,
+// [c0, c0 + CW) (CW = 128 / NP, part `part`) of key tile t (global keys from
+// kc), against the row's running (m, l). The NP parts exchange partial maxima
+// through the shared-memory slots at xslot and a named barrier.
+template <int D, int V, int NP>
+__device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int part,
                                               int kc, int lo, int hi, int t, uint32_t xslot,
                                               uint32_t bar_id, float sl2, uint64_t* s_full,
                                               uint64_t* p_full, Tracer& tr, int tkey) {
-  const int c0 = half * 64;
-  const int oc0 = half * (D / 2);
+  constexpr int CW = 128 / NP;
+  constexpr int OW = D / NP;  // output columns of this part (O rescale)
+  const int c0 = part * CW;
+  const int oc0 = part * OW;
   mbar_wait(s_full, t & 1);
   tr.ev(10, tkey);
   tc_fence_after();
-  uint32_t s[64];
-  tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&s[0]));
-  tmem_ld32(t_s + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&s[32]));
+  uint32_t s[CW];
+#pragma unroll
+  for (int c = 0; c < CW / 32; ++c) tmem_ld32(t_s + c0 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
   tmem_ld_wait();
-  const bool full = lo <= kc && kc + 64 <= hi;
+  const bool full = lo <= kc && kc + CW <= hi;
   if (!full) {
 #pragma unroll
-    for (int i = 0; i < 64; ++i) {
+    for (int i = 0; i < CW; ++i) {
       const int c = kc + i;
       if (c < lo || c >= hi) s[i] = __float_as_uint(-INFINITY);
     }
@@ -152,32 +167,36 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
 #pragma unroll
   for (int u = 0; u < 4; ++u) mx[u] = fmaxf(__uint_as_float(s[2 * u]), __uint_as_float(s[2 * u + 1]));
 #pragma unroll
-  for (int i = 8; i < 64; i += 8) {
+  for (int i = 8; i < CW; i += 8) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
   }
   const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-  asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + half * kSub * 4), "f"(pm) : "memory");
-  // both halves loaded S (P may now overwrite it) and published their max
-  named_bar_sync(bar_id, 256);
-  float po;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + (half ^ 1) * kSub * 4) : "memory");
-  const float mt = fmaxf(pm, po);
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + part * kSub * 4), "f"(pm) : "memory");
+  // every part published its max
+  named_bar_sync(bar_id, NP * 128);
+  float mt = pm;
+#pragma unroll
+  for (int o = 1; o < NP; ++o) {
+    float po;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + ((part + o) % NP) * kSub * 4) : "memory");
+    mt = fmaxf(mt, po);
+  }
   tr.ev(11, tkey);
   const float mt2 = mt * sl2;
   const bool move = mt2 > m + kRescaleThreshold;  // also true on the first finite tile
   const float alpha = move ? fast_exp2(m - mt2) : 1.f;
   if (move) m = mt2;
   const float mb = m == -INFINITY ? 0.f : m;
-  uint32_t pk[32];
+  uint32_t pk[CW / 2];
   float rs;
   if (full) {
     // packed f32x2: x = s * scale - m two lanes per FFMA2, sums by FADD2
     const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
     uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
-    for (int i = 0; i < 64; i += 2) {
+    for (int i = 0; i < CW; i += 2) {
       const int jj = i / 2;
       const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
       // pairs (jj % 8) on the FMA pipe: V0 {3, 7}, V1 {1, 4, 7}, V2 {7}
@@ -199,7 +218,7 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   } else {
     float rs4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int i = 0; i < 64; i += 2) {
+    for (int i = 0; i < CW; i += 2) {
       const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
       const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
       rs4[(i / 2) % 4] += p0 + p1;
@@ -209,11 +228,15 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   }
   l = l * alpha + rs;
   tr.ev(12, tkey);
-  // P (bf16 pairs): this half's 64 columns -> S columns [32 half, 32 half + 32)
-  tmem_st32(t_s + half * 32, pk);
+  // P (bf16 pairs) into the first CW/2 of this part's own (consumed) S columns
+  if constexpr (CW == 64) {
+    tmem_st32(t_s + c0, pk);
+  } else {
+    tmem_st16(t_s + c0, pk);
+  }
   if (t > 0 && __any_sync(0xffffffffu, move)) {
 #pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
+    for (int c = 0; c < OW / 32; ++c) {
       uint32_t o[32];
       tmem_ld32(t_o + oc0 + c * 32, o);
       tmem_ld_wait();
@@ -228,13 +251,14 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   tr.ev(13, tkey);
 }
 
-// Output of one sub-tile row half: normalise (or merge into an existing
-// (out, lse) pair) and store. lt = full row sum, lse_old read before any
-// half of this row stored the new lse.
-template <int D>
-__device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int q, int half, float m, float lt,
+// Output of one sub-tile row part (D / NP columns): normalise (or merge into
+// an existing (out, lse) pair) and store. lt = full row sum, lse_old read
+// before any part of this row stored the new lse.
+template <int D, int NP>
+__device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int q, int part, float m, float lt,
                                               float lse_old, uint32_t t_o, bool has_work, uint64_t* o_final) {
-  const int oc0 = half * (D / 2);
+  constexpr int OW = D / NP;
+  const int oc0 = part * OW;
   float* lse_ptr = p.lse + static_cast<size_t>(head) * p.seqlen_q + q;
   const bool valid = q < p.seqlen_q;
   const bool has = lt > 0.f;
@@ -254,7 +278,7 @@ __device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int 
     const float w_old = has ? __expf(lse_old - lse_new) : 1.f;
     const float w_cur = has ? __expf(lse_cur - lse_new) * inv_l : 0.f;
 #pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
+    for (int c = 0; c < OW / 32; ++c) {
       uint32_t o[32];
       if (has_work) {
         tmem_ld32(t_oh + c * 32, o);
@@ -273,10 +297,10 @@ __device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int 
         }
       }
     }
-    if (valid && has && half == 0) *lse_ptr = lse_new;
+    if (valid && has && part == 0) *lse_ptr = lse_new;
   } else {
 #pragma unroll 1
-    for (int c = 0; c < D / 64; ++c) {
+    for (int c = 0; c < OW / 32; ++c) {
       uint32_t o[32];
       if (has_work) {
         tmem_ld32(t_oh + c * 32, o);
@@ -307,20 +331,22 @@ __device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int 
         }
       }
     }
-    if (valid && half == 0) *lse_ptr = lse_cur;
+    if (valid && part == 0) *lse_ptr = lse_cur;
   }
 }
 
 // V: softmax variant (diagnostics, MAGI_FWD_VARIANT): exp2 pairs on the FMA
 // pipe out of every 8 — 0: 2 (25%), 1: 3 (37.5%), 2: 1 (12.5%).
-template <int D, int V, bool PAIR>
-__global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
+template <int D, int V, int LAYOUT>
+__global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
     ffa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k,
                    const __grid_constant__ CUtensorMap tmap_v, const FwdParams p) {
   using L = FwdSmem<D>;
-  constexpr int kTmaWarp = FwdLayout<PAIR>::kTmaWarp;
-  constexpr int kMmaWarp = FwdLayout<PAIR>::kMmaWarp;
+  constexpr bool PAIR = FwdLayout<LAYOUT>::kPair;
+  constexpr int NP = FwdLayout<LAYOUT>::kParts;
+  constexpr int kTmaWarp = FwdLayout<LAYOUT>::kTmaWarp;
+  constexpr int kMmaWarp = FwdLayout<LAYOUT>::kMmaWarp;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.s_full[i], 1);
-      mbar_init(&bars.p_full[i], 2 * kSub);
+      mbar_init(&bars.p_full[i], NP * kSub);
       mbar_init(&bars.o_final[i], 1);
     }
     fence_barrier_init();
@@ -446,7 +472,7 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
         mbar_wait(&bars.v_full[vst.index], vst.phase);
         tr.ev(2, t);
         tc_fence_after();
-        issue_pv<D>(tmem + 256, tmem + 0, v_desc, t > 0);
+        issue_pv<D, NP>(tmem + 256, tmem + 0, v_desc, t > 0);
         if (!more) umma_commit_elect(&bars.o_final[0]);
         const uint64_t k_desc = k_desc0 + kst.index * kStageDesc;
         if (more) {
@@ -460,7 +486,7 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
         mbar_wait(&bars.p_full[1], t & 1);
         tr.ev(4, t);
         tc_fence_after();
-        issue_pv<D>(tmem + 384, tmem + 128, v_desc, t > 0);
+        issue_pv<D, NP>(tmem + 384, tmem + 128, v_desc, t > 0);
         umma_commit_elect(&bars.v_empty[vst.index]);
         vst.advance<kStages>();
         if (!more) umma_commit_elect(&bars.o_final[1]);
@@ -475,29 +501,30 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
     }
   } else if (warp < kTmaWarp) {
     // ------------------------------------------------------------ softmax
-    // Thread = query row = TMEM lane; warpgroup half h owns score columns
-    // [64 h, 64 h + 64) of a sub-tile, and the two halves of a sub-tile
+    // Thread = query row = TMEM lane; warpgroup part w owns score columns
+    // [w 128/NP, (w+1) 128/NP) of a sub-tile, and the parts of a sub-tile
     // exchange partial row maxima through shared memory so they agree bit for
     // bit on the exponent base. PAIR: sub-tile = warp / 8, the two sub-tiles'
-    // phases overlap; otherwise both warpgroups walk both sub-tiles in turn.
+    // phases overlap; otherwise all warpgroups walk both sub-tiles in turn.
     if (PAIR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
     constexpr int kSubs = PAIR ? 1 : 2;  // sub-tiles this thread serves
     const int sub0 = PAIR ? warp / 8 : 0;
-    const int half = (warp / 4) & 1;
+    const int part = (warp / 4) % NP;
     const int row = (warp % 4) * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const float sl2 = p.scale_log2;
     const uint32_t xch_base = smem_u32(smem + L::kXch);
+    const uint32_t bar_n = PAIR ? 0 : 1;  // named barrier: per sub-tile (PAIR) or shared
     float m[kSubs], l[kSubs];
     int q[kSubs];
 #pragma unroll
     for (int u = 0; u < kSubs; ++u) {
       m[u] = -INFINITY;  // exponent base, log2 domain (lazily moved)
-      l[u] = 0.f;        // this half's sum of 2^(x - m)
+      l[u] = 0.f;        // this part's sum of 2^(x - m)
       q[u] = tile.q0 + (sub0 + u) * kSub + row;
     }
     Tracer tr;
-    if (half == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub0);
+    if (part == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub0);
     int t = 0;
     for (int it = tile.item_begin; it < tile.item_end; ++it) {
       const FwdItem item = p.items[it];
@@ -505,16 +532,16 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
 #pragma unroll
       for (int u = 0; u < kSubs; ++u) row_bounds(item.qs, item.qe, item.ks, item.ke, item.type, q[u], lo[u], hi[u]);
       for (int j = 0; j < item.n_ktiles; ++j, ++t) {
-        const int kc = item.k_begin + j * kBlockN + half * 64;
+        const int kc = item.k_begin + j * kBlockN + part * (128 / NP);
 #pragma unroll
         for (int u = 0; u < kSubs; ++u) {
           const int sub = sub0 + u;
-          // slot [t parity][sub][half][row]: a half can run one step ahead of
-          // the other's read, never two
-          const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 2) * kSub + row) * 4;
-          softmax_phase<D, V>(m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off, half,
-                              kc, lo[u], hi[u], t, xslot, PAIR ? 1 + sub : 1, sl2, &bars.s_full[sub],
-                              &bars.p_full[sub], tr, kSubs * t + u);
+          // slot [t parity][sub][part][row]: a part can run one step ahead of
+          // the others' reads, never two
+          const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 4) * kSub + row) * 4;
+          softmax_phase<D, V, NP>(m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off,
+                                  part, kc, lo[u], hi[u], t, xslot, PAIR ? 1 + sub : bar_n, sl2,
+                                  &bars.s_full[sub], &bars.p_full[sub], tr, kSubs * t + u);
         }
       }
     }
@@ -525,18 +552,20 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
     for (int u = 0; u < kSubs; ++u)
       lse_old[u] = (p.accumulate && q[u] < p.seqlen_q) ? p.lse[static_cast<size_t>(head) * p.seqlen_q + q[u]]
                                                       : -INFINITY;
-    // full row sums: this half's + the other half's; the barrier also orders
-    // every half's lse_old read before any lse store
-    float* xl = reinterpret_cast<float*>(smem + L::kXch) + 4 * 2 * kSub;  // [sub][half][row]
+    // full row sums over the parts; the barrier also orders every part's
+    // lse_old read before any lse store
+    float* xl = reinterpret_cast<float*>(smem + L::kXch) + L::kXl;  // [sub][part][row]
 #pragma unroll
-    for (int u = 0; u < kSubs; ++u) xl[((sub0 + u) * 2 + half) * kSub + row] = l[u];
-    named_bar_sync(PAIR ? 1 + sub0 : 1, 256);
+    for (int u = 0; u < kSubs; ++u) xl[((sub0 + u) * 4 + part) * kSub + row] = l[u];
+    named_bar_sync(PAIR ? 1 + sub0 : bar_n, NP * 128);
 #pragma unroll
     for (int u = 0; u < kSubs; ++u) {
       const int sub = sub0 + u;
-      const float lt = l[u] + xl[(sub * 2 + (half ^ 1)) * kSub + row];
-      softmax_store<D>(p, head, q[u], half, m[u], lt, lse_old[u], tmem + 256 + sub * 128 + lane_off, n_total > 0,
-                       &bars.o_final[sub]);
+      float lt = 0.f;
+#pragma unroll
+      for (int o = 0; o < NP; ++o) lt += xl[(sub * 4 + o) * kSub + row];
+      softmax_store<D, NP>(p, head, q[u], part, m[u], lt, lse_old[u], tmem + 256 + sub * 128 + lane_off,
+                           n_total > 0, &bars.o_final[sub]);
     }
   }
 
@@ -548,7 +577,7 @@ __global__ void __launch_bounds__(FwdLayout<PAIR>::kThreads, 1)
   }
 }
 
-template <int D, int V, bool PAIR>
+template <int D, int V, int LAYOUT>
 cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, const void* v,
                             cudaStream_t stream) {
   const CUtensorMap tq = make_tmap_thd(q, prm.seqlen_q, prm.hq, D, 128);
@@ -556,10 +585,10 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t err =
-      cudaFuncSetAttribute(ffa_fwd_kernel<D, V, PAIR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   const dim3 grid(static_cast<unsigned>(prm.num_tiles) * prm.hq);
-  ffa_fwd_kernel<D, V, PAIR><<<grid, FwdLayout<PAIR>::kThreads, smem, stream>>>(tq, tk, tv, prm);
+  ffa_fwd_kernel<D, V, LAYOUT><<<grid, FwdLayout<LAYOUT>::kThreads, smem, stream>>>(tq, tk, tv, prm);
   return cudaGetLastError();
 }
 
@@ -596,15 +625,17 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
   // for A/B runs: bit 0 = 640-thread layout, bits 1-2 = polynomial share.
   if (head_dim == 128) {
     switch (variant) {
-      case 1: return launch_fwd_impl<128, 0, true>(prm, q, k, v, stream);
-      case 3: return launch_fwd_impl<128, 1, true>(prm, q, k, v, stream);
-      case 4: return launch_fwd_impl<128, 0, false>(prm, q, k, v, stream);
-      case 5: return launch_fwd_impl<128, 2, true>(prm, q, k, v, stream);
-      case 6: return launch_fwd_impl<128, 2, false>(prm, q, k, v, stream);
-      default: return launch_fwd_impl<128, 1, false>(prm, q, k, v, stream);
+      case 1: return launch_fwd_impl<128, 0, 1>(prm, q, k, v, stream);
+      case 3: return launch_fwd_impl<128, 1, 1>(prm, q, k, v, stream);
+      case 4: return launch_fwd_impl<128, 0, 0>(prm, q, k, v, stream);
+      case 5: return launch_fwd_impl<128, 2, 1>(prm, q, k, v, stream);
+      case 6: return launch_fwd_impl<128, 2, 0>(prm, q, k, v, stream);
+      case 7: return launch_fwd_impl<128, 1, 2>(prm, q, k, v, stream);
+      case 8: return launch_fwd_impl<128, 0, 2>(prm, q, k, v, stream);
+      default: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
     }
   }
-  if (head_dim == 64) return launch_fwd_impl<64, 1, false>(prm, q, k, v, stream);
+  if (head_dim == 64) return launch_fwd_impl<64, 1, 0>(prm, q, k, v, stream);
   return cudaErrorInvalidValue;
 }
 
