@@ -38,7 +38,8 @@ def scenario(cp: int) -> dict:
     return {"workload": {"mask": {"seqlen": S, "pattern": "block_causal", "params": {"block_size": BLOCK}},
                          "num_heads_q": HQ, "num_heads_k": HK, "num_heads_v": HK, "head_dim": D},
             "cp_size": cp, "cost_model": COST,
-            "overlap": {"min_chunk_size": 4096, "max_num_chunks": 8}}
+            "overlap": {"min_chunk_size": 4096,
+                        "max_num_chunks": int(os.environ.get("MAGI_CP_MAX_CHUNKS", "8"))}}
 
 
 def run(args) -> None:

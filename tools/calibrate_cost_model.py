@@ -10,7 +10,11 @@ Samples, all in microseconds (the reference's cost units):
                      gather / scatter-add kernels around it — only when run
                      under torchrun with >= 2 ranks.
 Each set goes through the planner's own fit_affine (least squares, negative
-coefficients clamped), and rank 0 writes configs/cost_model_b200.json.
+coefficients clamped); the FFA latency terms are raised to the measured
+per-stage overhead (the same per-rank mask as one call vs split by key
+columns, stage_overhead_us), because a single call's intercept is ~0 while
+splitting the work into stages is not free. Rank 0 writes
+configs/cost_model_b200.json.
 
     python tools/calibrate_cost_model.py                      # FFA terms only
     torchrun --nproc-per-node 2 tools/calibrate_cost_model.py  # + cast/reduce
@@ -63,6 +67,59 @@ def ffa_samples(dev) -> tuple[list, list]:
     return fwd, bwd
 
 
+def stage_overhead_us(dev, S: int = 131072, block: int = 8192, pieces: int = 4) -> tuple[float, float]:
+    """Per-stage fixed cost of the FFA at the CP per-rank size: the same mask
+    run as one call vs split into `pieces` key-column ranges (the way stages
+    split the remote K/V), each piece merged with the fused LSE-merge /
+    accumulate epilogue. Returns (fwd, bwd) extra microseconds per piece."""
+    from paper_2505_13211_b200.planner import debug_eval
+
+    mask = {"seqlen": S, "pattern": "block_causal", "params": {"block_size": block}}
+    cs = S // pieces
+
+    def plan_of(col_chunks):
+        sl = debug_eval("chunk_pair_slices", mask=mask, chunk=cs, q_chunks=list(range(pieces)),
+                        k_chunks=col_chunks)
+        return FFAPlan([x[0:2] for x in sl], [x[2:4] for x in sl], [x[4] for x in sl], S,
+                       len(col_chunks) * cs, D) if sl else None
+
+    whole = plan_of(list(range(pieces)))
+    q = torch.randn(S, HQ, D, device=dev, dtype=torch.bfloat16)
+    k = torch.randn(S, HK, D, device=dev, dtype=torch.bfloat16)
+    v = torch.randn(S, HK, D, device=dev, dtype=torch.bfloat16)
+    do = torch.randn(S, HQ, D, device=dev, dtype=torch.bfloat16)
+    out = torch.zeros(S, HQ, D, device=dev, dtype=torch.float32)
+    lse = torch.full((HQ, S), float("-inf"), device=dev)
+    ks = [k[c * cs:(c + 1) * cs] for c in range(pieces)]
+    vs = [v[c * cs:(c + 1) * cs] for c in range(pieces)]
+    pk = [(pl, ks[c], vs[c]) for c, pl in enumerate(plan_of([c]) for c in range(pieces)) if pl is not None]
+
+    def fwd_whole():
+        ffa_forward(whole, q, k, v, out=out, lse=lse, accumulate=True)
+
+    def fwd_parts():
+        for pl, kk, vv in pk:
+            ffa_forward(pl, q, kk, vv, out=out, lse=lse, accumulate=True)
+
+    t1, tn = _time_us(fwd_whole, 2), _time_us(fwd_parts, 2)
+    o_bf, lse2 = ffa_forward(whole, q, k, v)
+    dq = torch.zeros(S, HQ, D, device=dev, dtype=torch.float32)
+    dk = torch.zeros(S, HK, D, device=dev, dtype=torch.float32)
+    dv = torch.zeros_like(dk)
+
+    def bwd_whole():
+        ffa_backward(whole, q, k, v, o_bf, lse2, do, dq=dq, dk=dk, dv=dv, accumulate=True)
+
+    def bwd_parts():
+        for c, (pl, kk, vv) in enumerate(pk):
+            ffa_backward(pl, q, kk, vv, o_bf, lse2, do, dq=dq, dk=dk[c * cs:(c + 1) * cs],
+                         dv=dv[c * cs:(c + 1) * cs], accumulate=True)
+
+    b1, bn = _time_us(bwd_whole, 2), _time_us(bwd_parts, 2)
+    n = len(pk)
+    return max(0.0, (tn - t1) / max(n - 1, 1)), max(0.0, (bn - b1) / max(n - 1, 1))
+
+
 def comm_samples(dev, world: int) -> tuple[list, list]:
     import torch.distributed as dist
 
@@ -94,9 +151,13 @@ def main() -> None:
     _lib.lib()
     model = {}
     fwd, bwd = ffa_samples(dev)
-    for name, samples in (("ffa_fwd", fwd), ("ffa_bwd", bwd)):
+    # the fitted intercept of a single call is ~0; what a stage really costs on
+    # top of its pairs is the split overhead, measured at the CP per-rank size
+    over_f, over_b = stage_overhead_us(dev)
+    for name, samples, over in (("ffa_fwd", fwd, over_f), ("ffa_bwd", bwd, over_b)):
         lat, per = debug_eval("fit_affine", samples=samples)
-        model[name] = {"latency": lat, "per_unit": per, "samples": samples}
+        model[name] = {"latency": max(lat, over), "per_unit": per, "samples": samples,
+                       "stage_overhead_us": over}
     if world > 1:
         import torch.distributed as dist
 

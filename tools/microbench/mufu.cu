@@ -42,6 +42,14 @@ __global__ void k(float* out, long long* clk, float seed) {
         pk[i] ^= pack_bf16(r[2 * i], r[2 * i + 1]);
         r[2 * i] = __uint_as_float(__float_as_uint(r[2 * i]) ^ pk[i]);
       }
+    } else if (OP == 5) {
+      // ex2.approx.f16x2: two exponentials per lane per instruction
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        uint32_t h = __float_as_uint(r[2 * i]);
+        asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
+        r[2 * i] = __uint_as_float(h);
+      }
     } else if (OP == 4) {
       // ex2 through the FMA-pipe polynomial, packed pairs
 #pragma unroll
@@ -88,6 +96,7 @@ int main() {
   run<2>("FFMA2", 8, out, clk);
   run<3>("F2FP+2xLOP", 8, out, clk);
   run<4>("exp2_poly2 (per pair)", 8, out, clk);
+  run<5>("MUFU.EX2 f16x2 (per pair)", 8, out, clk);
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
