@@ -107,13 +107,29 @@ def stage_overhead_us(dev, S: int = 131072, block: int = 8192, pieces: int = 4) 
     dk = torch.zeros(S, HK, D, device=dev, dtype=torch.float32)
     dv = torch.zeros_like(dk)
 
+    # as the CP executor runs a stage: delta once per pass, then dQ (accumulate)
+    # and a fresh f32 dK/dV partial per stage
+    L = _lib.lib()
+    sp = torch.cuda.current_stream(dev).cuda_stream
+    delta = torch.empty((HQ, S), dtype=torch.float32, device=dev)
+    _lib.check(L.magiplan_ffa_bwd_preprocess(o_bf.data_ptr(), do.data_ptr(), delta.data_ptr(), S, HQ, D,
+                                             _lib.BF16, sp))
+    scale = D ** -0.5
+
+    def bwd_calls(pl, kk, vv, dkk, dvv):
+        _lib.check(L.magiplan_ffa_bwd_dq(pl.handle, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), lse2.data_ptr(),
+                                         delta.data_ptr(), do.data_ptr(), dq.data_ptr(), HQ, HK, scale,
+                                         _lib.F32, 1, sp))
+        _lib.check(L.magiplan_ffa_bwd_dkdv(pl.handle, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), lse2.data_ptr(),
+                                           delta.data_ptr(), do.data_ptr(), dkk.data_ptr(), dvv.data_ptr(), HQ,
+                                           HK, scale, _lib.F32, 0, sp))
+
     def bwd_whole():
-        ffa_backward(whole, q, k, v, o_bf, lse2, do, dq=dq, dk=dk, dv=dv, accumulate=True)
+        bwd_calls(whole, k, v, dk, dv)
 
     def bwd_parts():
         for c, (pl, kk, vv) in enumerate(pk):
-            ffa_backward(pl, q, kk, vv, o_bf, lse2, do, dq=dq, dk=dk[c * cs:(c + 1) * cs],
-                         dv=dv[c * cs:(c + 1) * cs], accumulate=True)
+            bwd_calls(pl, kk, vv, dk[c * cs:(c + 1) * cs], dv[c * cs:(c + 1) * cs])
 
     b1, bn = _time_us(bwd_whole, 2), _time_us(bwd_parts, 2)
     n = len(pk)
