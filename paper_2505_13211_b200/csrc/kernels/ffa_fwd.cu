@@ -154,6 +154,7 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
 #pragma unroll
   for (int c = 0; c < CW / 32; ++c) tmem_ld32(t_s + c0 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
   tmem_ld_wait();
+  tr.ev(14, tkey);
   const bool full = lo <= kc && kc + CW <= hi;
   if (!full) {
 #pragma unroll
@@ -174,6 +175,7 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   }
   const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + part * kSub * 4), "f"(pm) : "memory");
+  tr.ev(15, tkey);
   // every part published its max
   named_bar_sync(bar_id, NP * 128);
   float mt = pm;

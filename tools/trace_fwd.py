@@ -75,7 +75,8 @@ def main(block: int = 0):
                   if (a, t + off) in evr and (b, t) in evr]
             return statistics.median(xs) if xs else float("nan")
 
-        print(f"WG{role - 1}: S ready->regs {g2(10, 11):.0f} | regs->exp {g2(11, 12):.0f} | "
+        print(f"WG{role - 1}: S ready->ld done {g2(10, 14):.0f} | ->max stored {g2(14, 15):.0f} | "
+              f"->barrier passed {g2(15, 11):.0f} | ->exp done {g2(11, 12):.0f} | "
               f"exp->P written {g2(12, 13):.0f} | P written(t-1)->S ready(t) {g2(13, 10, -1):.0f} ns")
         print("   " + " ".join(f"{(evr[(10, t)] - t0) / 1e3:.2f}/{(evr[(13, t)] - t0) / 1e3:.2f}"
                            for t in range(3, min(steps, 9)) if (10, t) in evr and (13, t) in evr))
