@@ -218,15 +218,19 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
     const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
     rs = a2.x + a2.y;
   } else {
-    float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+    // masked scores are -inf: all exponentials on MUFU (exact zeros), packed
+    // arithmetic otherwise as above
+    const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
+    uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
 #pragma unroll
     for (int i = 0; i < CW; i += 2) {
-      const float p0 = fast_exp2(fmaf(__uint_as_float(s[i]), sl2, -mb));
-      const float p1 = fast_exp2(fmaf(__uint_as_float(s[i + 1]), sl2, -mb));
-      rs4[(i / 2) % 4] += p0 + p1;
+      const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
+      const float p0 = fast_exp2(x.x), p1 = fast_exp2(x.y);
+      acc2[(i / 2) % 4] = fadd2(acc2[(i / 2) % 4], f2(p0, p1));
       pk[i / 2] = pack_bf16(p0, p1);
     }
-    rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+    const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
+    rs = a2.x + a2.y;
   }
   l = l * alpha + rs;
   tr.ev(12, tkey);
