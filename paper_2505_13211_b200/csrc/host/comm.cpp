@@ -61,16 +61,26 @@ std::vector<KvDemand> compute_kv_demands(const AttnMask& m, const DispatchPlan& 
   }
   const Token cs = plan.chunk_size;
   const std::size_t cp = static_cast<std::size_t>(plan.cp_size);
-  // need[kc * cp + r]: rank r owns a row attending a column of kv chunk kc
-  std::vector<uint8_t> need(static_cast<std::size_t>(n) * cp, 0);
-  visit_row_unions(m, [&](Token q, const std::vector<TokenRange>& iv) {
+  const std::size_t stride = static_cast<std::size_t>(n) + 1;
+  // cover[owner * (n+1) + kc]: difference array of the kv-chunk intervals the
+  // owner's rows attend (O(1) per row interval instead of O(chunks))
+  std::vector<int64_t> cover(cp * stride, 0);
+  sweep_row_unions(m, [&](Token q, const std::vector<TokenRange>& iv) {
     const auto owner = static_cast<std::size_t>(plan.assignment[static_cast<std::size_t>(q / cs)]);
     for (const TokenRange& r : iv) {
-      for (int64_t kc = r.start / cs; kc <= (r.end - 1) / cs; ++kc) {
-        need[static_cast<std::size_t>(kc) * cp + owner] = 1;
-      }
+      cover[owner * stride + static_cast<std::size_t>(r.start / cs)] += 1;
+      cover[owner * stride + static_cast<std::size_t>((r.end - 1) / cs) + 1] -= 1;
     }
   });
+  // need[kc * cp + r]: rank r owns a row attending a column of kv chunk kc
+  std::vector<uint8_t> need(static_cast<std::size_t>(n) * cp, 0);
+  for (std::size_t r = 0; r < cp; ++r) {
+    int64_t run = 0;
+    for (int64_t kc = 0; kc < n; ++kc) {
+      run += cover[r * stride + static_cast<std::size_t>(kc)];
+      if (run > 0) need[static_cast<std::size_t>(kc) * cp + r] = 1;
+    }
+  }
   std::vector<KvDemand> out(static_cast<std::size_t>(n));
   for (int64_t kc = 0; kc < n; ++kc) {
     KvDemand& d = out[static_cast<std::size_t>(kc)];

@@ -179,33 +179,11 @@ Pairs merge_intervals(std::vector<TokenRange>& iv) {
 
 }  // namespace
 
-void visit_row_unions(const AttnMask& m, const RowVisitor& fn) {
-  std::vector<std::size_t> order(m.slices.size());
-  std::iota(order.begin(), order.end(), 0);
-  std::stable_sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
-    return m.slices[x].q.start < m.slices[y].q.start;
-  });
-  std::vector<std::size_t> live;
-  std::vector<TokenRange> iv;
-  std::size_t next = 0;
-  for (Token q = 0; q < m.seqlen_q; ++q) {
-    for (; next < order.size() && m.slices[order[next]].q.start <= q; ++next) {
-      if (m.slices[order[next]].q.end > q) live.push_back(order[next]);
-    }
-    std::erase_if(live, [&](std::size_t i) { return m.slices[i].q.end <= q; });
-    iv.clear();
-    for (std::size_t i : live) {
-      const TokenRange c = m.slices[i].cols(q);
-      if (!c.empty()) iv.push_back(c);
-    }
-    merge_intervals(iv);
-    fn(q, iv);
-  }
-}
+void visit_row_unions(const AttnMask& m, const RowVisitor& fn) { sweep_row_unions(m, fn); }
 
 std::vector<Pairs> union_row_counts(const AttnMask& m) {
   std::vector<Pairs> counts(static_cast<std::size_t>(std::max<Token>(0, m.seqlen_q)), 0);
-  visit_row_unions(m, [&](Token q, const std::vector<TokenRange>& iv) {
+  sweep_row_unions(m, [&](Token q, const std::vector<TokenRange>& iv) {
     Pairs n = 0;
     for (const auto& r : iv) n += r.length();
     counts[static_cast<std::size_t>(q)] = n;

@@ -14,7 +14,9 @@
 #pragma once
 
 #include <cstdint>
+#include <algorithm>
 #include <functional>
+#include <limits>
 #include <optional>
 #include <string>
 #include <vector>
@@ -84,6 +86,55 @@ AttnMask restrict_rows(const AttnMask& m, const std::vector<TokenRange>& rows);
 // Visit every query row's merged allowed column intervals, in row order.
 using RowVisitor = std::function<void(Token, const std::vector<TokenRange>&)>;
 void visit_row_unions(const AttnMask& m, const RowVisitor& fn);
+
+// Inline form of the same sweep for the hot planner loops (no per-row
+// indirect call; the live-slice set is only pruned when a slice ends).
+template <class F>
+void sweep_row_unions(const AttnMask& m, F&& fn) {
+  std::vector<std::size_t> order(m.slices.size());
+  for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) {
+    return m.slices[x].q.start < m.slices[y].q.start;
+  });
+  std::vector<std::size_t> live;
+  std::vector<TokenRange> iv;
+  std::size_t next = 0;
+  Token first_end = std::numeric_limits<Token>::max();  // smallest q.end among live slices
+  for (Token q = 0; q < m.seqlen_q; ++q) {
+    for (; next < order.size() && m.slices[order[next]].q.start <= q; ++next) {
+      const AttnSlice& s = m.slices[order[next]];
+      if (s.q.end > q) {
+        live.push_back(order[next]);
+        first_end = std::min(first_end, s.q.end);
+      }
+    }
+    if (q >= first_end) {
+      std::erase_if(live, [&](std::size_t i) { return m.slices[i].q.end <= q; });
+      first_end = std::numeric_limits<Token>::max();
+      for (std::size_t i : live) first_end = std::min(first_end, m.slices[i].q.end);
+    }
+    iv.clear();
+    for (std::size_t i : live) {
+      const TokenRange c = m.slices[i].cols(q);
+      if (!c.empty()) iv.push_back(c);
+    }
+    if (iv.size() > 1) {
+      std::sort(iv.begin(), iv.end(), [](const TokenRange& x, const TokenRange& y) {
+        return x.start != y.start ? x.start < y.start : x.end < y.end;
+      });
+      std::size_t w = 0;
+      for (std::size_t i = 1; i < iv.size(); ++i) {
+        if (iv[i].start <= iv[w].end) {
+          iv[w].end = std::max(iv[w].end, iv[i].end);
+        } else {
+          iv[++w] = iv[i];
+        }
+      }
+      iv.resize(w + 1);
+    }
+    fn(q, iv);
+  }
+}
 std::vector<Pairs> union_row_counts(const AttnMask& m);
 std::vector<TokenRange> row_union(const AttnMask& m, Token q);
 
