@@ -70,6 +70,7 @@ struct BwdParams {
   int32_t lse_tma;      // lse / delta rows fetched by TMA (row stride 16B-aligned)
   long long* trace;     // diagnostics: event log of one CTA (nullptr = off)
   int32_t trace_block;
+  int32_t trace_kernel;  // 0: dK/dV kernel, 1: dQ kernel (MAGI_TRACE_DQ)
 };
 
 long long* g_trace = nullptr;
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   const int head_k = head / (p.hq / p.hk);
   const FwdTile tile = p.q_tiles[tile_rank];
   const int steps = tile.n_ktiles;
+  long long* const trace = static_cast<int>(blockIdx.x) == p.trace_block && p.trace_kernel == 1 ? p.trace : nullptr;
 
   if (threadIdx.x == 0) {
     mbar_init(&bars.qdo_full, kDqMath);
@@ -309,6 +311,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             umma_ts_elect(d_tmem, a_tmem + k * 8, desc_add(b_desc, (k / 4) * kBox + (k % 4) * 32), idesc_s, k > 0);
         }
       };
+      Tracer tr;
+      if (lane == 0) tr.init(trace, 0);
+      tr.clk(98);
       mbar_wait(&bars.qdo_full, 0);
       PipeState nst, gst;
       mbar_wait(&bars.k_full[nst.index], nst.phase);
@@ -324,6 +329,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const bool more = t + 1 < steps;
         if (more) {
           mbar_wait(&bars.s_free, t & 1);
+          tr.ev(1, t);
           mbar_wait(&bars.k_full[nst.index], nst.phase);
           mbar_wait(&bars.v_full[nst.index], nst.phase);
           tc_fence_after();
@@ -331,6 +337,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           umma_commit_elect(&bars.s_full);
         }
         mbar_wait(&bars.p_full, t & 1);
+        tr.ev(2, t);
         tc_fence_after();
         // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys
         // [32w, 32w+32) at column 32w), B = K [keys, D] MN-major
@@ -343,10 +350,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           umma_commit_elect(&bars.dp_full);
           umma_commit_elect(&bars.v_empty[nst.index]);
           nst.advance<S>();
+          tr.ev(3, t);
         } else {
           umma_commit_elect(&bars.done);
         }
       }
+      tr.clk(99);
     }
   } else if (warp < kDqTmaWarp) {
     // four warpgroups split the 128 key columns: wg w takes [32w, 32w+32)
@@ -367,6 +376,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       tc_fence_before();
       mbar_arrive(&bars.qdo_full);
     }
+    Tracer tr;
+    if (warp % 4 == 0 && lane == 0 && wg < 2) tr.init(trace, 1 + wg);
     float lse_l2 = INFINITY, dlt = 0.f;
     if (valid) {
       const float raw = p.lse[static_cast<size_t>(head) * p.seqlen_q + q];
@@ -381,6 +392,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       for (int j = 0; j < item.n_ktiles; ++j, ++t) {
         const int k0 = item.k_begin + j * kBlockN;
         mbar_wait(&bars.s_full, t & 1);
+        tr.ev(10, t);
         tc_fence_after();
         if (p.experiment == 1) {
           tc_fence_before();
@@ -424,7 +436,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             }
           }
         }
+        tr.ev(11, t);
         mbar_wait(&bars.dp_full, t & 1);
+        tr.ev(12, t);
         tc_fence_after();
         {
           uint32_t dp[32], ds[16];
@@ -444,6 +458,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         tmem_st_wait();
         tc_fence_before();
         mbar_arrive(&bars.p_full);
+        tr.ev(13, t);
       }
     }
     if (steps > 0) {
@@ -542,6 +557,11 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.num_q_tiles = num_q_tiles;
   prm.trace = g_trace;
   prm.trace_block = g_trace_block;
+  static const bool trace_dq = [] {
+    const char* e = std::getenv("MAGI_TRACE_DQ");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  prm.trace_kernel = trace_dq ? 1 : 0;
   prm.dout = grad_out;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
