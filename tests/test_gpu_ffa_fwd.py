@@ -77,3 +77,36 @@ def test_fwd_deterministic(built_lib, cuda):
     o2, l2 = ffa_forward(plan, q, k, v)
     torch.cuda.synchronize()
     assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("gain", [4.0, 12.0])
+def test_fwd_bwd_large_logits(built_lib, cuda, gain):
+    """Scores spread over tens of log2 units: the lazily moved softmax base is
+    rescaled often (row maxima keep growing along the key walk) and the
+    FMA-pipe exp2 sees arguments far below -126."""
+    from oracle import oracle
+    from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward
+
+    sq = sk = 768
+    hq, hk, d = 2, 1, 128
+    qr, kr, ty = [[0, 768]], [[0, 768]], [1]  # causal: the key walk meets larger maxima late
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=3)
+    # keys with growing norm along the sequence push row maxima up tile after tile
+    ramp = torch.linspace(0.2, 1.0, sk, device=q.device)[:, None, None]
+    q = (q.float() * gain).to(torch.bfloat16)
+    k = (k.float() * ramp).to(torch.bfloat16)
+    plan = FFAPlan(qr, kr, ty, sq, sk, d)
+    out, lse = ffa_forward(plan, q, k, v)
+    dq, dk, dv = ffa_backward(plan, q, k, v, out, lse, do)
+    torch.cuda.synchronize()
+    scale = 1.0 / math.sqrt(d)
+    ref_o, ref_lse = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale)
+    o_abs, o_rel = err_stats(out.float().cpu().numpy(), ref_o)
+    l_abs, _ = err_stats(lse.cpu().numpy(), ref_lse)
+    assert o_abs <= O_ABS * 2 and o_rel <= O_REL * 2, (o_abs, o_rel)
+    assert l_abs <= LSE_ABS * gain, l_abs
+    rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ref_o, ref_lse, do, qr, kr, ty, scale)
+    for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        _, rel = err_stats(got.float().cpu().numpy(), ref)
+        assert rel <= 4e-2, rel
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
