@@ -6,21 +6,23 @@
 // Overlapping slices are merged inside the CTA (MULTIPLICITY semantics,
 // reference proj/include/magiplan/mask.hpp:85): no atomics.
 //
-// Warp roles (320 threads):
-//   warps 0-3 / 4-7  softmax, score columns [0,64) / [64,128) of BOTH
-//                    sub-tiles (thread = query row = TMEM lane): the two
-//                    warpgroups process one sub-tile together, exchange their
-//                    partial row maxima through shared memory, apply the slice
-//                    row bounds, run the online softmax with a lazily moved max
-//                    (rescale O only when the row max grows by > 2^8), exp2
-//                    split between MUFU and an FFMA2 polynomial, and write P
-//                    back into the S columns as packed bf16 (tcgen05.st).
+// Warp roles (default layout 5, 384 threads; the alternatives below are kept
+// for A/B runs):
+//   warps 0-3 / 4-7  softmax of sub-tile 0 / 1, thread = one full 128-column
+//                    query row = TMEM lane (no cross-warp max exchange): apply
+//                    the slice row bounds, online softmax with a lazily moved
+//                    max (rescale O only when the row max grows by > 2^8),
+//                    exp2 split between MUFU and an FFMA2 polynomial, P back
+//                    into the S columns as packed bf16 (tcgen05.st). setmaxnreg
+//                    gives these warps 200 registers.
 //   warp 8           TMA producer: Q once, K/V through a 2-stage ring.
-//   warp 9           MMA issuer (one lane). Per key tile t:
+//   warp 9           MMA issuer (converged warp, one elected lane). Per key
+//                    tile t:
 //                      S0 = Q0 K^T, S1 = Q1 K^T           (SS, M=128 N=128)
 //                      O0 += P0 V, then S0' = Q0 K'^T      (P from TMEM: TS)
 //                      O1 += P1 V, then S1' = Q1 K'^T
 //                    so softmax of one sub-tile overlaps the MMAs of the other.
+//   warps 10-11      idle (complete the control warpgroup for setmaxnreg).
 // TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,384) O1 [384,512).
 // Issue order guarantees: S_i(t+1) is issued after O_i += P_i(t) V, so when a
 // softmax thread sees S_i(t+1) complete, P_i(t)'s MMA has retired and O_i is
@@ -51,14 +53,24 @@ constexpr int kSub = 128;                // rows per sub-tile
 //      1 control warp x 56 <= 5 x 96.
 //   2: 576 threads, NP = 4: four warpgroups (32 columns each) walk both
 //      sub-tiles one after the other; warp 16 TMA, warp 17 MMA.
-constexpr uint32_t kSoftmaxRegs = 104;
+//   4: 320 threads, NP = 1: one warpgroup per sub-tile, thread = a full
+//      128-column row (no max exchange), the two sub-tiles ping-pong;
+//      warp 8 TMA, warp 9 MMA.
+//   5: as 4 with a control warpgroup (warps 8-11: TMA, MMA, 2 idle) so
+//      setmaxnreg can give the softmax warps 200 registers (2 x 200 + 96 <=
+//      3 x 168 per SM sub-partition).
+constexpr uint32_t kSoftmaxRegs = 104;  // layout 1
 constexpr uint32_t kControlRegs = 56;
 template <int LAYOUT>
 struct FwdLayout {
-  static constexpr bool kPair = LAYOUT == 1;
-  static constexpr int kParts = LAYOUT == 2 ? 4 : 2;
-  static constexpr int kThreads = LAYOUT == 0 ? 320 : (LAYOUT == 1 ? 640 : 576);
-  static constexpr int kTmaWarp = LAYOUT == 0 ? 8 : 16;
+  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || LAYOUT == 5;  // one sub-tile per warpgroup set
+  static constexpr bool kSetmaxnreg = LAYOUT == 1 || LAYOUT == 5;
+  static constexpr uint32_t kSoftRegs = LAYOUT == 5 ? 200 : kSoftmaxRegs;
+  static constexpr uint32_t kCtrlRegs = LAYOUT == 5 ? 96 : kControlRegs;
+  static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || LAYOUT == 5) ? 1 : 2);
+  static constexpr int kThreads =
+      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : (LAYOUT == 5 ? 384 : 576));
+  static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || LAYOUT == 5) ? 8 : 16;
   static constexpr int kMmaWarp = kTmaWarp + 1;
 };
 constexpr float kLog2e = 1.4426950408889634f;
@@ -126,7 +138,9 @@ __device__ __forceinline__ void issue_qk(uint32_t tmem_s, uint64_t q_desc, uint6
 template <int D, int NP>
 __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint64_t v_desc, bool accumulate) {
   constexpr uint32_t idesc = make_idesc_bf16(128, D, false, true);
-  if constexpr (NP == 2) {
+  if constexpr (NP == 1) {
+    umma_gemm_ts_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
+  } else if constexpr (NP == 2) {
     umma_gemm_ts_dq_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
   } else {
     umma_gemm_ts_dkdv_k128(tmem_o, tmem_p, v_desc, idesc, accumulate ? 1u : 0u);
@@ -174,11 +188,13 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
       mx[u] = fmaxf(mx[u], fmaxf(__uint_as_float(s[i + 2 * u]), __uint_as_float(s[i + 2 * u + 1])));
   }
   const float pm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+  float mt = pm;
+  if constexpr (NP > 1) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + part * kSub * 4), "f"(pm) : "memory");
   tr.ev(15, tkey);
   // every part published its max
   named_bar_sync(bar_id, NP * 128);
-  float mt = pm;
+  }
 #pragma unroll
   for (int o = 1; o < NP; ++o) {
     float po;
@@ -235,7 +251,10 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   l = l * alpha + rs;
   tr.ev(12, tkey);
   // P (bf16 pairs) into the first CW/2 of this part's own (consumed) S columns
-  if constexpr (CW == 64) {
+  if constexpr (CW == 128) {
+    tmem_st32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+    tmem_st32(t_s + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
+  } else if constexpr (CW == 64) {
     tmem_st32(t_s + c0, pk);
   } else {
     tmem_st16(t_s + c0, pk);
@@ -394,7 +413,8 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
 
-  if (PAIR && warp >= kTmaWarp) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kControlRegs));
+  if (FwdLayout<LAYOUT>::kSetmaxnreg && warp >= kTmaWarp)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FwdLayout<LAYOUT>::kCtrlRegs));
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_total > 0) {
@@ -430,7 +450,7 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
         }
       }
     }
-  } else if (PAIR && warp == kMmaWarp + 1) {
+  } else if (FwdLayout<LAYOUT>::kThreads == 640 && warp == kMmaWarp + 1) {
     // diagnostics only: observe when K / V tiles land (traced CTA)
     if (lane == 0 && trace != nullptr && n_total > 0) {
       Tracer tr;
@@ -512,9 +532,10 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
     // exchange partial row maxima through shared memory so they agree bit for
     // bit on the exponent base. PAIR: sub-tile = warp / 8, the two sub-tiles'
     // phases overlap; otherwise all warpgroups walk both sub-tiles in turn.
-    if (PAIR) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kSoftmaxRegs));
+    if (FwdLayout<LAYOUT>::kSetmaxnreg)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FwdLayout<LAYOUT>::kSoftRegs));
     constexpr int kSubs = PAIR ? 1 : 2;  // sub-tiles this thread serves
-    const int sub0 = PAIR ? warp / 8 : 0;
+    const int sub0 = PAIR ? warp / (4 * NP) : 0;
     const int part = (warp / 4) % NP;
     const int row = (warp % 4) * 32 + lane;
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
@@ -626,9 +647,10 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
     const char* e = std::getenv("MAGI_FWD_VARIANT");
     return e ? std::atoi(e) : 0;
   }();
-  // default: 320-thread layout, 37.5% of the exponentials on the FMA pipe
-  // (measured best on config 2); MAGI_FWD_VARIANT selects the alternatives
-  // for A/B runs: bit 0 = 640-thread layout, bits 1-2 = polynomial share.
+  // default: layout 5 (full-row softmax warpgroups with 200 registers via
+  // setmaxnreg), 25% of the exponentials on the FMA pipe — measured best on
+  // config 2 (~4% over layout 0); MAGI_FWD_VARIANT selects the alternatives
+  // for A/B runs.
   if (head_dim == 128) {
     switch (variant) {
       case 1: return launch_fwd_impl<128, 0, 1>(prm, q, k, v, stream);
@@ -638,7 +660,12 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
       case 6: return launch_fwd_impl<128, 2, 0>(prm, q, k, v, stream);
       case 7: return launch_fwd_impl<128, 1, 2>(prm, q, k, v, stream);
       case 8: return launch_fwd_impl<128, 0, 2>(prm, q, k, v, stream);
-      default: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
+      case 10: return launch_fwd_impl<128, 0, 4>(prm, q, k, v, stream);
+      case 11: return launch_fwd_impl<128, 1, 4>(prm, q, k, v, stream);
+      case 12: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
+      case 13: return launch_fwd_impl<128, 1, 5>(prm, q, k, v, stream);
+      case 14: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
+      default: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
     }
   }
   if (head_dim == 64) return launch_fwd_impl<64, 1, 0>(prm, q, k, v, stream);
