@@ -16,11 +16,14 @@ using namespace magi;
 constexpr int kIters = 2048;
 
 // FORM 0: SS, 1: TS, 2: TS with B MN-major (the P.V form), 3: SS with B MN-major
-template <int FORM, int N>
+// LOADERS: warps 1..3 keep reading TMEM columns [384, 512) meanwhile
+template <int FORM, int N, bool LOADERS = false>
 __global__ void __launch_bounds__(128, 1) k(long long* clk) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t done;
   __shared__ uint32_t slot;
+  __shared__ int stop_flag;
+  if (threadIdx.x == 0) stop_flag = 0;
   const int warp = threadIdx.x / 32;
   for (int i = threadIdx.x; i < (64 * 1024) / 16; i += blockDim.x)
     reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
@@ -58,6 +61,17 @@ __global__ void __launch_bounds__(128, 1) k(long long* clk) {
     mbar_wait(&done, 0);
     long long c1 = clock64();
     clk[blockIdx.x] = c1 - c0;
+    stop_flag = 1;
+  } else if (LOADERS && threadIdx.x >= 32) {
+    uint32_t acc = 0;
+    const uint32_t t = tmem + (static_cast<uint32_t>((warp % 4) * 32) << 16) + 384;
+    for (int it = 0; it < 20000 && !*(volatile int*)&stop_flag; ++it) {
+      uint32_t r[32];
+      tmem_ld32(t + (it & 3) * 32, r);
+      tmem_ld_wait();
+      acc ^= r[0] ^ r[31];
+    }
+    if (acc == 12345u) clk[1] = acc;
   }
   tc_fence_before();
   __syncthreads();
@@ -67,15 +81,15 @@ __global__ void __launch_bounds__(128, 1) k(long long* clk) {
   }
 }
 
-template <int FORM, int N>
+template <int FORM, int N, bool LOADERS = false>
 void run(const char* name, long long* clk) {
-  cudaFuncSetAttribute(k<FORM, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  k<FORM, N><<<148, 128, 65536>>>(clk);
+  cudaFuncSetAttribute(k<FORM, N, LOADERS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  k<FORM, N, LOADERS><<<148, 128, 65536>>>(clk);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  k<FORM, N><<<148, 128, 65536>>>(clk);
+  k<FORM, N, LOADERS><<<148, 128, 65536>>>(clk);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -98,6 +112,8 @@ int main() {
   run<1, 128>("TS", clk);
   run<2, 128>("TS B-MN", clk);
   run<3, 128>("SS B-MN", clk);
+  run<0, 128, true>("SS +TMEM ld", clk);
+  run<2, 128, true>("TS B-MN +TMEM ld", clk);
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }

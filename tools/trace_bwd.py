@@ -58,6 +58,8 @@ def main(block: int = 0):
     for w in (0, 1):
         print(f"wg{w}: S ready->P written {gap(10, 11):.0f} | P->dP ready {gap(11, 12):.0f} | "
               f"dP ready->dS written {gap(12, 13):.0f} | dS written(t-1)->S ready(t) {gap(13, 10, -1):.0f} ns")
+    print(f"exp phase: S ready->S in regs {gap(10, 14):.0f} | ->P packed {gap(14, 15):.0f} | "
+          f"->P stored {gap(15, 16):.0f} | ->arrived {gap(16, 11):.0f} ns")
     print(f"mma: P ready->Q(t+1) landed {gap(1, 2):.0f} | Q landed->dS ready {gap(2, 3):.0f} | "
           f"dS ready->dO(t+1) landed {gap(3, 4):.0f} ns")
     for t in range(3, min(steps, 6)):
