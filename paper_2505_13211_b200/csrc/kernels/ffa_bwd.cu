@@ -212,15 +212,8 @@ __device__ __forceinline__ void stage_row_to_tmem(const __nv_bfloat16* base, int
   }
 }
 
-// dQ kernel layout: 4 elementwise warpgroups (32 key columns each) + TMA warp
-// + MMA warp
-constexpr int kDqThreads = 576;
-constexpr int kDqTmaWarp = 16;
-constexpr int kDqMmaWarp = 17;
-constexpr int kDqMath = 512;
-
-template <int D>
-__global__ void __launch_bounds__(kDqThreads, 1)
+template <int D, bool TR>
+__global__ void __launch_bounds__(kThreads, 1)
     ffa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmap_q,
                       const __grid_constant__ CUtensorMap tmap_k,
                       const __grid_constant__ CUtensorMap tmap_v,
@@ -245,7 +238,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   long long* const trace = static_cast<int>(blockIdx.x) == p.trace_block && p.trace_kernel == 1 ? p.trace : nullptr;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bars.qdo_full, kDqMath);
+    mbar_init(&bars.qdo_full, kMath);
     for (int s = 0; s < S; ++s) {
       mbar_init(&bars.k_full[s], 1);
       mbar_init(&bars.k_empty[s], 1);
@@ -253,13 +246,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       mbar_init(&bars.v_empty[s], 1);
     }
     mbar_init(&bars.s_full, 1);
-    mbar_init(&bars.s_free, kDqMath);
+    mbar_init(&bars.s_free, kMath);
     mbar_init(&bars.dp_full, 1);
-    mbar_init(&bars.p_full, kDqMath);
+    mbar_init(&bars.p_full, kMath);
     mbar_init(&bars.done, 1);
     fence_barrier_init();
   }
-  if (warp == kDqMmaWarp) tmem_alloc<512>(&tmem_slot);
+  if (warp == kMmaWarp) tmem_alloc<512>(&tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -270,7 +263,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   uint8_t* sK = smem + L::kK;
   uint8_t* sV = smem + L::kV;
 
-  if (warp == kDqTmaWarp) {
+  if (warp == kTmaWarp) {
     if (lane == 0 && steps > 0) {
       tma_prefetch_desc(&tmap_k);
       tma_prefetch_desc(&tmap_v);
@@ -293,7 +286,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
       }
     }
-  } else if (warp == kDqMmaWarp) {
+  } else if (warp == kMmaWarp) {
     // converged warp; one elected lane issues every MMA / commit
     if (steps > 0) {
       constexpr uint32_t idesc_s = make_idesc_bf16(128, 128, false, false);
@@ -311,8 +304,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             umma_ts_elect(d_tmem, a_tmem + k * 8, desc_add(b_desc, (k / 4) * kBox + (k % 4) * 32), idesc_s, k > 0);
         }
       };
-      Tracer tr;
-      if (lane == 0) tr.init(trace, 0);
+      TracerT<TR> tr;
+      tr.init(trace, 0);  // uniform across the converged warp
       tr.clk(98);
       mbar_wait(&bars.qdo_full, 0);
       PipeState nst, gst;
@@ -339,9 +332,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         mbar_wait(&bars.p_full, t & 1);
         tr.ev(2, t);
         tc_fence_after();
-        // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys
-        // [32w, 32w+32) at column 32w), B = K [keys, D] MN-major
-        if (p.experiment != 2) umma_gemm_ts_dkdv_k128(t_dq, t_dp, k_mn0 + gst.index * kStageDesc, idesc_q, t > 0 ? 1u : 0u);
+        // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys [0,64)
+        // at +0, keys [64,128) at +64), B = K [keys, D] MN-major
+        if (p.experiment != 2) umma_gemm_ts_dq_k128(t_dq, t_dp, k_mn0 + gst.index * kStageDesc, idesc_q, t > 0 ? 1u : 0u);
         umma_commit_elect(&bars.k_empty[gst.index]);
         gst.advance<S>();
         if (more) {
@@ -357,27 +350,27 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
       tr.clk(99);
     }
-  } else if (warp < kDqTmaWarp) {
-    // four warpgroups split the 128 key columns: wg w takes [32w, 32w+32)
+  } else {
+    // two warpgroups split the 128 key columns: wg 0 [0, 64), wg 1 [64, 128)
     const int wg = warp / 4;
-    const int col0 = wg * 32;
+    const int col0 = wg * 64;
     const int row = (warp % 4) * 32 + lane;
     const int q = tile.q0 + row;
     const uint32_t lane_off = static_cast<uint32_t>((warp % 4) * 32) << 16;
     const bool valid = q < p.seqlen_q;
     const float sl2 = p.scale_log2;
     if (steps > 0) {
-      // stage Q and dO rows into TMEM (each warpgroup a quarter of the head dim)
-      stage_row_to_tmem<D, D / 4>(static_cast<const __nv_bfloat16*>(p.q), p.hq, head, q, valid,
-                                  wg * (D / 4), t_q + lane_off + wg * (D / 8));
-      stage_row_to_tmem<D, D / 4>(static_cast<const __nv_bfloat16*>(p.dout), p.hq, head, q, valid,
-                                  wg * (D / 4), t_do + lane_off + wg * (D / 8));
+      // stage Q and dO rows into TMEM (each warpgroup half of the head dim)
+      stage_row_to_tmem<D, D / 2>(static_cast<const __nv_bfloat16*>(p.q), p.hq, head, q, valid,
+                           wg * (D / 2), t_q + lane_off + wg * (D / 4));
+      stage_row_to_tmem<D, D / 2>(static_cast<const __nv_bfloat16*>(p.dout), p.hq, head, q, valid,
+                           wg * (D / 2), t_do + lane_off + wg * (D / 4));
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars.qdo_full);
     }
-    Tracer tr;
-    if (warp % 4 == 0 && lane == 0 && wg < 2) tr.init(trace, 1 + wg);
+    TracerT<TR> tr;
+    if (warp % 4 == 0) tr.init(trace, 1 + wg);
     float lse_l2 = INFINITY, dlt = 0.f;
     if (valid) {
       const float raw = p.lse[static_cast<size_t>(head) * p.seqlen_q + q];
@@ -402,37 +395,42 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           mbar_arrive(&bars.p_full);
           continue;
         }
-        float pv[32];
+        float pv[64];
         {
           const int kb = k0 + col0;
-          const bool all_in = lo <= kb && kb + 32 <= hi;
-          uint32_t s[32];
-          tmem_ld32(t_s + lane_off + col0, s);
-          tmem_ld_wait();
-          tc_fence_before();
-          mbar_arrive(&bars.s_free);
-          if (all_in) {
-            // x = s * scale * log2e - lse * log2e, two lanes per FFMA2; a
-            // quarter of the exponentials on the FMA pipe
-            const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
+          const bool all_in = lo <= kb && kb + 64 <= hi;
 #pragma unroll
-            for (int c = 0; c < 32; c += 2) {
-              const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
-              if (c % 8 == 6) {
-                const float2 e = exp2_poly2(x.x, x.y);
-                pv[c] = e.x;
-                pv[c + 1] = e.y;
-              } else {
-                pv[c] = fast_exp2(x.x);
-                pv[c + 1] = fast_exp2(x.y);
-              }
+          for (int h2 = 0; h2 < 2; ++h2) {
+            uint32_t s[32];
+            tmem_ld32(t_s + lane_off + col0 + h2 * 32, s);
+            tmem_ld_wait();
+            if (h2 == 1) {
+              tc_fence_before();
+              mbar_arrive(&bars.s_free);
             }
-          } else {
+            if (all_in) {
+              // x = s * scale * log2e - lse * log2e, two lanes per FFMA2; a
+              // quarter of the exponentials on the FMA pipe
+              const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int kk = kb + c;
-              const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
-              pv[c] = (kk >= lo && kk < hi) ? e : 0.f;
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
+                if (c % 8 == 6) {
+                  const float2 e = exp2_poly2(x.x, x.y);
+                  pv[h2 * 32 + c] = e.x;
+                  pv[h2 * 32 + c + 1] = e.y;
+                } else {
+                  pv[h2 * 32 + c] = fast_exp2(x.x);
+                  pv[h2 * 32 + c + 1] = fast_exp2(x.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 32; ++c) {
+                const int kk = kb + h2 * 32 + c;
+                const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
+                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? e : 0.f;
+              }
             }
           }
         }
@@ -440,20 +438,22 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         mbar_wait(&bars.dp_full, t & 1);
         tr.ev(12, t);
         tc_fence_after();
-        {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
           uint32_t dp[32], ds[16];
-          tmem_ld32(t_dp + lane_off + col0, dp);
+          tmem_ld32(t_dp + lane_off + col0 + c * 32, dp);
           tmem_ld_wait();
           const uint64_t nd2 = f2(-dlt, -dlt);
 #pragma unroll
           for (int j2 = 0; j2 < 32; j2 += 2) {
+            const int col = c * 32 + j2;
             // dS = P (dP - delta): FADD2 + FMUL2 per pair
-            const float2 d = f2_split(fmul2(f2(pv[j2], pv[j2 + 1]),
+            const float2 d = f2_split(fmul2(f2(pv[col], pv[col + 1]),
                                             fadd2(f2(__uint_as_float(dp[j2]), __uint_as_float(dp[j2 + 1])), nd2)));
             ds[j2 / 2] = pack_bf16(d.x, d.y);
           }
-          // dS -> the first 16 of this warpgroup's 32 consumed dP columns
-          tmem_st16(t_dp + lane_off + col0, ds);
+          // dS chunk -> this warpgroup's consumed dP columns [col0 + c*16, +16)
+          tmem_st16(t_dp + lane_off + col0 + c * 16, ds);
         }
         tmem_st_wait();
         tc_fence_before();
@@ -465,18 +465,15 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       mbar_wait(&bars.done, 0);
       tc_fence_after();
     }
-    // each warpgroup writes a quarter of the dQ row (D = 64: two warpgroups, halves)
-    constexpr int kEpi = D >= 128 ? D / 4 : 32;
-    if (wg * kEpi < D) {
-      const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + wg * kEpi;
-      epilogue_rows<kEpi>(t_dq + lane_off + wg * kEpi, steps > 0, valid, p.dq, row_off, p.scale,
-                          p.grad_f32 != 0, p.accumulate != 0);
-    }
+    // each warpgroup writes half of the dQ row
+    const size_t row_off = (static_cast<size_t>(q) * p.hq + head) * D + wg * (D / 2);
+    epilogue_rows<D / 2>(t_dq + lane_off + wg * (D / 2), steps > 0, valid, p.dq, row_off, p.scale,
+                         p.grad_f32 != 0, p.accumulate != 0);
   }
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kDqMmaWarp) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc<512>(tmem);
   }
@@ -498,8 +495,10 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       return e ? std::atoi(e) : 0;
     }();
     // default 37.5% of the exponentials on the FMA pipe (measured best)
-    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0>
-                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2> : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3> : ffa_bwd_dkdv_kernel<D, 1>));
+    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0, false>
+                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2, false>
+                                       : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3, false> : ffa_bwd_dkdv_kernel<D, 1, false>));
+    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true>;  // diagnostics
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
@@ -517,10 +516,11 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   }
   if ((parts & 2) && num_q_tiles > 0) {
     const int smem = DqSmem<D>::kBytes + 1024;
-    err = cudaFuncSetAttribute(ffa_bwd_dq_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto dq_kern = prm.trace != nullptr && prm.trace_kernel == 1 ? ffa_bwd_dq_kernel<D, true> : ffa_bwd_dq_kernel<D, false>;
+    err = cudaFuncSetAttribute(dq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
-    ffa_bwd_dq_kernel<D><<<dim3(num_q_tiles * prm.hq), kDqThreads, smem, stream>>>(tq, tk, tv, tdo,
+    dq_kern<<<dim3(num_q_tiles * prm.hq), kThreads, smem, stream>>>(tq, tk, tv, tdo,
                                                                                  prm);
     err = cudaGetLastError();
   }

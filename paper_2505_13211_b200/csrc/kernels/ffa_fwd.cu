@@ -152,11 +152,11 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint6
 // [c0, c0 + CW) (CW = 128 / NP, part `part`) of key tile t (global keys from
 // kc), against the row's running (m, l). The NP parts exchange partial maxima
 // through the shared-memory slots at xslot and a named barrier.
-template <int D, int V, int NP>
+template <int D, int V, int NP, class TRC>
 __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int part,
                                               int kc, int lo, int hi, int t, uint32_t xslot,
                                               uint32_t bar_id, float sl2, uint64_t* s_full,
-                                              uint64_t* p_full, Tracer& tr, int tkey) {
+                                              uint64_t* p_full, TRC& tr, int tkey) {
   constexpr int CW = 128 / NP;
   constexpr int OW = D / NP;  // output columns of this part (O rescale)
   const int c0 = part * CW;
@@ -362,7 +362,7 @@ __device__ __forceinline__ void softmax_store(const FwdParams& p, int head, int 
 
 // V: softmax variant (diagnostics, MAGI_FWD_VARIANT): exp2 pairs on the FMA
 // pipe out of every 8 — 0: 2 (25%), 1: 3 (37.5%), 2: 1 (12.5%).
-template <int D, int V, int LAYOUT>
+template <int D, int V, int LAYOUT, bool TR>
 __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
     ffa_fwd_kernel(const __grid_constant__ CUtensorMap tmap_q,
                    const __grid_constant__ CUtensorMap tmap_k,
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
   if (warp == kTmaWarp) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0 && n_total > 0) {
-      Tracer tr;
+      TracerT<TR> tr;
       tr.init(trace, 3);
       int tt = 0;
       tma_prefetch_desc(&tmap_q);
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
   } else if (FwdLayout<LAYOUT>::kThreads == 640 && warp == kMmaWarp + 1) {
     // diagnostics only: observe when K / V tiles land (traced CTA)
     if (lane == 0 && trace != nullptr && n_total > 0) {
-      Tracer tr;
+      TracerT<TR> tr;
       tr.init(trace, 4);
       PipeState st;
       for (int t = 0; t < n_total; ++t) {
@@ -473,8 +473,8 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
       const uint64_t k_desc0 = make_smem_desc(smem_u32(sK), 16, 1024);
       const uint64_t v_desc0 = make_smem_desc(smem_u32(sV), kBox, 1024);
       constexpr uint32_t kStageDesc = L::kTileBytes >> 4;  // stage stride in descriptor units
-      Tracer tr;
-      if (lane == 0) tr.init(trace, 0);
+      TracerT<TR> tr;
+      tr.init(trace, 0);  // uniform across the converged warp
       tr.clk(98);
       mbar_wait(&bars.q_full, 0);
       PipeState kst, vst;
@@ -550,8 +550,8 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
       l[u] = 0.f;        // this part's sum of 2^(x - m)
       q[u] = tile.q0 + (sub0 + u) * kSub + row;
     }
-    Tracer tr;
-    if (part == 0 && warp % 4 == 0 && lane == 0) tr.init(trace, 1 + sub0);
+    TracerT<TR> tr;
+    if (part == 0 && warp % 4 == 0) tr.init(trace, 1 + sub0);
     int t = 0;
     for (int it = tile.item_begin; it < tile.item_end; ++it) {
       const FwdItem item = p.items[it];
@@ -612,10 +612,19 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
   const CUtensorMap tv = make_tmap_thd(v, prm.seqlen_k, prm.hk, D, 128);
   const int smem = FwdSmem<D>::kBytes + 1024;
   cudaError_t err =
-      cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   const dim3 grid(static_cast<unsigned>(prm.num_tiles) * prm.hq);
-  ffa_fwd_kernel<D, V, LAYOUT><<<grid, FwdLayout<LAYOUT>::kThreads, smem, stream>>>(tq, tk, tv, prm);
+  if constexpr (V == 0 && LAYOUT == 5) {
+    if (prm.trace != nullptr) {  // diagnostics: the traced instantiation of the default kernel
+      err = cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+      if (err != cudaSuccess) return err;
+      ffa_fwd_kernel<D, V, LAYOUT, true><<<grid, FwdLayout<LAYOUT>::kThreads, smem, stream>>>(tq, tk, tv, prm);
+      return cudaGetLastError();
+    }
+  }
+  ffa_fwd_kernel<D, V, LAYOUT, false><<<grid, FwdLayout<LAYOUT>::kThreads, smem, stream>>>(tq, tk, tv, prm);
   return cudaGetLastError();
 }
 

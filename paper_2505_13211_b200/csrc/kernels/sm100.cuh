@@ -305,29 +305,40 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 // Per-role event log (diagnostics, magiplan_debug_set_trace): role r writes
 // {event << 32 | step, %globaltimer ns} pairs into its own region, no atomics.
 constexpr int kTraceCap = 8000;
-struct Tracer {
+// ON = false compiles to nothing: production kernels are instantiated without
+// tracing (a not-taken trace call still splits basic blocks and costs
+// scheduling freedom in the hot loops); the traced instantiation is launched
+// only while magiplan_debug_set_trace is active.
+template <bool ON>
+struct TracerT {
   long long* base = nullptr;
   int n = 0;
   __device__ __forceinline__ void init(long long* trace, int role) {
-    base = trace ? trace + 1 + static_cast<size_t>(role) * 2 * kTraceCap : nullptr;
+    if constexpr (ON) base = trace ? trace + 1 + static_cast<size_t>(role) * 2 * kTraceCap : nullptr;
   }
   __device__ __forceinline__ void ev(int e, int t) {
-    if (base == nullptr || n >= kTraceCap) return;
-    unsigned long long ns;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-    base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(t);
-    base[2 * n + 1] = static_cast<long long>(ns);
-    ++n;
+    if constexpr (ON) {
+      if (base == nullptr || n >= kTraceCap) return;
+      if ((threadIdx.x & 31) != 0) return;  // lane 0 writes (converged callers init every lane)
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(t);
+      base[2 * n + 1] = static_cast<long long>(ns);
+      ++n;
+    }
   }
   // {event << 32 | low 32 bits of clock64, ns}: two of these give the SM clock
   __device__ __forceinline__ void clk(int e) {
-    if (base == nullptr || n >= kTraceCap) return;
-    unsigned long long ns;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-    const long long c = clock64();
-    base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(c);
-    base[2 * n + 1] = static_cast<long long>(ns);
-    ++n;
+    if constexpr (ON) {
+      if (base == nullptr || n >= kTraceCap) return;
+      if ((threadIdx.x & 31) != 0) return;
+      unsigned long long ns;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+      const long long c = clock64();
+      base[2 * n] = (static_cast<long long>(e) << 32) | static_cast<unsigned>(c);
+      base[2 * n + 1] = static_cast<long long>(ns);
+      ++n;
+    }
   }
 };
 
