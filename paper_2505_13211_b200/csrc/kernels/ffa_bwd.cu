@@ -494,11 +494,21 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       const char* e = std::getenv("MAGI_BWD_POLY");
       return e ? std::atoi(e) : 0;
     }();
+    static const int nw = [] {
+      const char* e = std::getenv("MAGI_DKV_WARPGROUPS");
+      return e && std::atoi(e) == 2 ? 2 : 4;
+    }();
     // default 37.5% of the exponentials on the FMA pipe (measured best)
-    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0, false>
-                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2, false>
-                                       : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3, false> : ffa_bwd_dkdv_kernel<D, 1, false>));
-    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true>;  // diagnostics
+    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0, false, 4>
+                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2, false, 4>
+                                       : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3, false, 4> : ffa_bwd_dkdv_kernel<D, 1, false, 4>));
+    int threads = DkvLayout<4>::kThreads;
+    if (nw == 2) {
+      kern = ffa_bwd_dkdv_kernel<D, 1, false, 2>;
+      threads = DkvLayout<2>::kThreads;
+    }
+    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, 4>;  // diagnostics
+    if (prm.trace != nullptr && prm.trace_kernel == 0 && nw == 2) kern = ffa_bwd_dkdv_kernel<D, 1, true, 2>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
@@ -509,7 +519,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
       td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
     }
-    kern<<<dim3(num_k_tiles * prm.hk), kDkvThreads, smem, stream>>>(tq, tk, tv, tdo, tl,
+    kern<<<dim3(num_k_tiles * prm.hk), threads, smem, stream>>>(tq, tk, tv, tdo, tl,
                                                                                    td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
