@@ -425,11 +425,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
               }
             } else {
+              // packed arithmetic, all exponentials on MUFU, masked keys selected to zero
+              const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
 #pragma unroll
-              for (int c = 0; c < 32; ++c) {
+              for (int c = 0; c < 32; c += 2) {
+                const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
                 const int kk = kb + h2 * 32 + c;
-                const float e = fast_exp2(fmaf(__uint_as_float(s[c]), sl2, -lse_l2));
-                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? e : 0.f;
+                const float e0 = fast_exp2(x.x), e1 = fast_exp2(x.y);
+                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? e0 : 0.f;
+                pv[h2 * 32 + c + 1] = (kk + 1 >= lo && kk + 1 < hi) ? e1 : 0.f;
               }
             }
           }
