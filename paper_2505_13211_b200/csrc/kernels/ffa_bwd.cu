@@ -212,7 +212,9 @@ __device__ __forceinline__ void stage_row_to_tmem(const __nv_bfloat16* base, int
   }
 }
 
-template <int D, bool TR>
+// PQ: share of the exponentials on the FMA pipe (pairs out of 8): 0 = 2/8,
+// 1 = 3/8 (default, measured best), 2 = 1/8, 3 = 4/8 (A/B knob MAGI_DQ_POLY)
+template <int D, bool TR, int PQ = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     ffa_bwd_dq_kernel(const __grid_constant__ CUtensorMap tmap_q,
                       const __grid_constant__ CUtensorMap tmap_k,
@@ -415,7 +417,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
               for (int c = 0; c < 32; c += 2) {
                 const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
-                if (c % 8 == 6) {
+                constexpr uint32_t kPolyMask = PQ == 0 ? 0x88u : (PQ == 1 ? 0x92u : (PQ == 2 ? 0x80u : 0xAAu));
+                if ((kPolyMask >> ((c / 2) % 8)) & 1u) {
                   const float2 e = exp2_poly2(x.x, x.y);
                   pv[h2 * 32 + c] = e.x;
                   pv[h2 * 32 + c + 1] = e.y;
@@ -530,7 +533,14 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   }
   if ((parts & 2) && num_q_tiles > 0) {
     const int smem = DqSmem<D>::kBytes + 1024;
-    auto dq_kern = prm.trace != nullptr && prm.trace_kernel == 1 ? ffa_bwd_dq_kernel<D, true> : ffa_bwd_dq_kernel<D, false>;
+    static const int dq_poly = [] {
+      const char* e = std::getenv("MAGI_DQ_POLY");
+      return e ? std::atoi(e) : 1;
+    }();
+    auto dq_kern = dq_poly == 0 ? ffa_bwd_dq_kernel<D, false, 0>
+                                : (dq_poly == 2 ? ffa_bwd_dq_kernel<D, false, 2>
+                                                : (dq_poly == 3 ? ffa_bwd_dq_kernel<D, false, 3> : ffa_bwd_dq_kernel<D, false, 1>));
+    if (prm.trace != nullptr && prm.trace_kernel == 1) dq_kern = ffa_bwd_dq_kernel<D, true, 1>;
     err = cudaFuncSetAttribute(dq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                smem);
     if (err != cudaSuccess) return err;
