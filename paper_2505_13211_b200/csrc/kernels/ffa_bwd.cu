@@ -514,6 +514,11 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       kern = ffa_bwd_dkdv_kernel<D, 1, false, 2>;
       threads = DkvLayout<2>::kThreads;
     }
+    static const bool sched_y = [] {
+      const char* e = std::getenv("MAGI_DKV_SCHED");
+      return e != nullptr && std::atoi(e) == 1;
+    }();
+    if (sched_y) kern = nw == 2 ? ffa_bwd_dkdv_kernel<D, 1, false, 2, true> : ffa_bwd_dkdv_kernel<D, 1, false, 4, true>;
     if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, 4>;  // diagnostics
     if (prm.trace != nullptr && prm.trace_kernel == 0 && nw == 2) kern = ffa_bwd_dkdv_kernel<D, 1, true, 2>;
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
