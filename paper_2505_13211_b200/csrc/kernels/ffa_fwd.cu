@@ -63,14 +63,15 @@ constexpr uint32_t kSoftmaxRegs = 104;  // layout 1
 constexpr uint32_t kControlRegs = 56;
 template <int LAYOUT>
 struct FwdLayout {
-  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || LAYOUT == 5;  // one sub-tile per warpgroup set
-  static constexpr bool kSetmaxnreg = LAYOUT == 1 || LAYOUT == 5;
-  static constexpr uint32_t kSoftRegs = LAYOUT == 5 ? 200 : kSoftmaxRegs;
-  static constexpr uint32_t kCtrlRegs = LAYOUT == 5 ? 96 : kControlRegs;
-  static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || LAYOUT == 5) ? 1 : 2);
+  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6;
+  static constexpr bool kSetmaxnreg = LAYOUT == 1 || LAYOUT == 5 || LAYOUT == 6;
+  static constexpr bool kSplitP = LAYOUT == 6;  // layout 5 + P handed to the MMA in two key halves
+  static constexpr uint32_t kSoftRegs = (LAYOUT == 5 || LAYOUT == 6) ? 200 : kSoftmaxRegs;
+  static constexpr uint32_t kCtrlRegs = (LAYOUT == 5 || LAYOUT == 6) ? 96 : kControlRegs;
+  static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6) ? 1 : 2);
   static constexpr int kThreads =
-      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : (LAYOUT == 5 ? 384 : 576));
-  static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || LAYOUT == 5) ? 8 : 16;
+      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : ((LAYOUT == 5 || LAYOUT == 6) ? 384 : 576));
+  static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6) ? 8 : 16;
   static constexpr int kMmaWarp = kTmaWarp + 1;
 };
 constexpr float kLog2e = 1.4426950408889634f;
@@ -113,6 +114,7 @@ struct FwdBarriers {
   uint64_t k_full[kStages], k_empty[kStages];
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2], o_final[2];
+  uint64_t p_first[2];  // split P hand-off: keys [0,64) of P stored (layout 6)
 };
 
 // S = Q K^T (SS, both K-major): descriptors of the two tiles' first k-step;
@@ -152,11 +154,12 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint6
 // [c0, c0 + CW) (CW = 128 / NP, part `part`) of key tile t (global keys from
 // kc), against the row's running (m, l). The NP parts exchange partial maxima
 // through the shared-memory slots at xslot and a named barrier.
-template <int D, int V, int NP, class TRC>
+template <int D, int V, int NP, class TRC, bool SPLITP = false>
 __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int part,
                                               int kc, int lo, int hi, int t, uint32_t xslot,
                                               uint32_t bar_id, float sl2, uint64_t* s_full,
-                                              uint64_t* p_full, TRC& tr, int tkey) {
+                                              uint64_t* p_full, TRC& tr, int tkey,
+                                              uint64_t* p_first = nullptr) {
   constexpr int CW = 128 / NP;
   constexpr int OW = D / NP;  // output columns of this part (O rescale)
   const int c0 = part * CW;
@@ -207,6 +210,56 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
   const float alpha = move ? fast_exp2(m - mt2) : 1.f;
   if (move) m = mt2;
   const float mb = m == -INFINITY ? 0.f : m;
+  if constexpr (SPLITP) {
+    static_assert(NP == 1, "the split P hand-off is for full-row phases");
+    // O rescale first: the MMA may start P V on the first key half before
+    // this phase ends (O is quiescent: S(t) done implies P(t-1) V done)
+    if (t > 0 && __any_sync(0xffffffffu, move)) {
+#pragma unroll 1
+      for (int c = 0; c < OW / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(t_o + c * 32, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+        tmem_st32(t_o + c * 32, o);
+      }
+    }
+    const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-mb, -mb);
+    float rs = 0.f;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      uint32_t pk[32];
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+      for (int i = 64 * h; i < 64 * h + 64; i += 2) {
+        const int jj = i / 2;
+        const float2 x = f2_split(ffma2(f2(__uint_as_float(s[i]), __uint_as_float(s[i + 1])), sc2, nm2));
+        constexpr uint32_t kPolyMask = V == 0 ? 0x88u : (V == 1 ? 0x92u : 0x80u);
+        float p0, p1;
+        if (full && ((kPolyMask >> (jj % 8)) & 1u)) {
+          const float2 e = exp2_poly2(x.x, x.y);
+          p0 = e.x;
+          p1 = e.y;
+        } else {
+          p0 = fast_exp2(x.x);  // masked scores are -inf: exact zeros
+          p1 = fast_exp2(x.y);
+        }
+        acc2[jj % 4] = fadd2(acc2[jj % 4], f2(p0, p1));
+        pk[jj - 32 * h] = pack_bf16(p0, p1);
+      }
+      const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
+      rs += a2.x + a2.y;
+      // this key half of P into its S columns, then hand it to the MMA warp
+      tmem_st32(t_s + 32 * h, pk);
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(h == 0 ? p_first : p_full);
+    }
+    l = l * alpha + rs;
+    tr.ev(13, tkey);
+    return;
+  }
   uint32_t pk[CW / 2];
   float rs;
   if (full) {
@@ -399,6 +452,7 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&bars.s_full[i], 1);
       mbar_init(&bars.p_full[i], NP * kSub);
+      mbar_init(&bars.p_first[i], NP * kSub);
       mbar_init(&bars.o_final[i], 1);
     }
     fence_barrier_init();
@@ -493,12 +547,25 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
         const bool more = t + 1 < n_total;
         const uint64_t v_desc = v_desc0 + vst.index * kStageDesc;
         // sub-tile 0: O0 += P0 V, then S0 for the next key tile
+        if constexpr (FwdLayout<LAYOUT>::kSplitP) {
+          // P V by key halves, each as soon as its half of P is in TMEM
+          constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, false, true);
+          mbar_wait(&bars.v_full[vst.index], vst.phase);
+          mbar_wait(&bars.p_first[0], t & 1);
+          tc_fence_after();
+          umma_gemm_ts_k128_lo(tmem + 256, tmem + 0, v_desc, idesc_pv, t > 0 ? 1u : 0u);
+          mbar_wait(&bars.p_full[0], t & 1);
+          tr.ev(1, t);
+          tc_fence_after();
+          umma_gemm_ts_k128_hi(tmem + 256, tmem + 0, v_desc, idesc_pv, 1u);
+        } else {
         mbar_wait(&bars.p_full[0], t & 1);
         tr.ev(1, t);
         mbar_wait(&bars.v_full[vst.index], vst.phase);
         tr.ev(2, t);
         tc_fence_after();
         issue_pv<D, NP>(tmem + 256, tmem + 0, v_desc, t > 0);
+        }
         if (!more) umma_commit_elect(&bars.o_final[0]);
         const uint64_t k_desc = k_desc0 + kst.index * kStageDesc;
         if (more) {
@@ -509,10 +576,21 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
           umma_commit_elect(&bars.s_full[0]);
         }
         // sub-tile 1
+        if constexpr (FwdLayout<LAYOUT>::kSplitP) {
+          constexpr uint32_t idesc_pv = make_idesc_bf16(128, D, false, true);
+          mbar_wait(&bars.p_first[1], t & 1);
+          tc_fence_after();
+          umma_gemm_ts_k128_lo(tmem + 384, tmem + 128, v_desc, idesc_pv, t > 0 ? 1u : 0u);
+          mbar_wait(&bars.p_full[1], t & 1);
+          tr.ev(4, t);
+          tc_fence_after();
+          umma_gemm_ts_k128_hi(tmem + 384, tmem + 128, v_desc, idesc_pv, 1u);
+        } else {
         mbar_wait(&bars.p_full[1], t & 1);
         tr.ev(4, t);
         tc_fence_after();
         issue_pv<D, NP>(tmem + 384, tmem + 128, v_desc, t > 0);
+        }
         umma_commit_elect(&bars.v_empty[vst.index]);
         vst.advance<kStages>();
         if (!more) umma_commit_elect(&bars.o_final[1]);
@@ -566,9 +644,10 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
           // slot [t parity][sub][part][row]: a part can run one step ahead of
           // the others' reads, never two
           const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 4) * kSub + row) * 4;
-          softmax_phase<D, V, NP>(m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off,
-                                  part, kc, lo[u], hi[u], t, xslot, PAIR ? 1 + sub : bar_n, sl2,
-                                  &bars.s_full[sub], &bars.p_full[sub], tr, kSubs * t + u);
+          softmax_phase<D, V, NP, TracerT<TR>, FwdLayout<LAYOUT>::kSplitP>(
+              m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off, part, kc, lo[u], hi[u], t,
+              xslot, PAIR ? 1 + sub : bar_n, sl2, &bars.s_full[sub], &bars.p_full[sub], tr, kSubs * t + u,
+              &bars.p_first[sub]);
         }
       }
     }
@@ -673,6 +752,7 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
       case 11: return launch_fwd_impl<128, 1, 4>(prm, q, k, v, stream);
       case 12: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
       case 13: return launch_fwd_impl<128, 1, 5>(prm, q, k, v, stream);
+      case 15: return launch_fwd_impl<128, 0, 6>(prm, q, k, v, stream);
       case 14: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
       default: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
     }

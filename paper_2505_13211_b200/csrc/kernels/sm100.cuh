@@ -285,6 +285,21 @@ MAGI_TS_GEMM(umma_gemm_ts_bk_k128, 0, 8, 16, 24, 32, 40, 48, 56, 0, 2, 4, 6, 102
 MAGI_TS_GEMM(umma_gemm_ts_dkdv_k128, 0, 8, 32, 40, 64, 72, 96, 104, 0, 128, 256, 384, 512, 640, 768, 896)
 // A: the dQ kernel's packed dS layout: keys [0,64) at +0, [64,128) at +64; B MN-major
 MAGI_TS_GEMM(umma_gemm_ts_dq_k128, 0, 8, 16, 24, 64, 72, 80, 88, 0, 128, 256, 384, 512, 640, 768, 896)
+// half-depth (K = 64) forms of the consecutive-A / MN-major-B GEMM: keys
+// [0,64) and [64,128) of a 128-key tile (the forward's split P hand-off)
+#define MAGI_TS_GEMM4(name, a0, a1, a2, a3, b0, b1, b2, b3)                                      \
+  __device__ __forceinline__ void name(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,        \
+                                       uint32_t idesc, uint32_t accumulate) {                   \
+    asm volatile("{\n .reg .pred p, t, e;\n .reg .b32 a;\n .reg .b64 b;\n"                    \
+                 " setp.ne.b32 p, %4, 0;\n setp.eq.b32 t, %4, %4;\n"                          \
+                 " elect.sync _|e, 0xffffffff;\n" MAGI_TS_STEP(a0, b0, "p")                   \
+                     MAGI_TS_STEP(a1, b1, "t") MAGI_TS_STEP(a2, b2, "t") MAGI_TS_STEP(a3, b3, "t") \
+                 "}" ::"r"(d_tmem), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)        \
+                 : "memory");                                                                   \
+  }
+MAGI_TS_GEMM4(umma_gemm_ts_k128_lo, 0, 8, 16, 24, 0, 128, 256, 384)
+MAGI_TS_GEMM4(umma_gemm_ts_k128_hi, 32, 40, 48, 56, 512, 640, 768, 896)
+#undef MAGI_TS_GEMM4
 #undef MAGI_TS_GEMM
 
 // descriptor of the same tile advanced by `bytes` (start address field only)
