@@ -4,30 +4,24 @@
 // kernels so every gradient element has exactly one producing CTA and one
 // fixed accumulation order:
 //
-//   dkdv kernel (k-major): one CTA per (128-key tile, key/value head), walking
-//     every (q head of the GQA group, slice item, 128-query tile) that touches
-//     its keys:
-//       S^T  = K Q^T,  dP^T = V dO^T                     (TMEM)
-//       P^T  = exp2(S^T c - lse)   kept in registers, then packed bf16 into
-//                                  the consumed dP^T columns (TMEM)
-//       dS^T = P^T (dP^T - delta) -> smem (bf16)
-//       dV  += P^T dO  (A from TMEM)   dK += dS^T Q  (A from smem)
+//   dK/dV kernel (k-major, ffa_bwd_dkdv.inc): one CTA per (128-key tile,
+//     key/value head), walking every (q head of the GQA group, slice item,
+//     128-query tile) that touches its keys:
+//       S^T = K Q^T, dP^T = V dO^T (SS) into TMEM; P^T into the consumed S^T
+//       columns, dS^T = P^T (dP^T - delta) into the consumed dP^T columns
+//       (packed bf16); dV += P^T dO, dK += dS^T Q (TS, A from TMEM).
 //     dK / dV accumulate in TMEM over the whole walk and are written once.
-//   dq kernel (q-major): one CTA per (128-query tile, q head) over the
-//     forward work list: S = Q K^T, dP = dO V^T, dS = P (dP - delta) -> smem,
-//     dQ += dS K (TMEM).
+//   dQ kernel (q-major, below): one CTA per (128-query tile, q head) over the
+//     forward work list, Q and dO staged once into TMEM: S = Q K^T,
+//     dP = dO V^T, dS = P (dP - delta) into the consumed dP columns,
+//     dQ += dS K — all three TS.
 //
-// Overlap comes from issue order, not extra accumulators (TMEM is full): the
-// elementwise warps signal "S consumed" as soon as S(t) sits in registers, so
-// the MMA warp issues S(t+1) while they exponentiate; the gradient MMAs of
-// step t follow, then dP(t+1) into the dP region they just released. Every
-// other hand-off is implied by in-order MMA completion (dP(t+1) done => the
-// gradient MMAs of step t, which read the dS smem tile and the P columns,
-// retired). All MMAs are M=128, N=128 (or N=D), K=16: at that shape the SS
-// operand traffic stays within the shared-memory port.
-//
-// Warp roles in both: warps 0-3 elementwise (thread = TMEM lane = one row),
-// warp 4 TMA producer, warp 5 MMA issuer.
+// Overlap comes from issue order, not extra accumulators (TMEM is full); every
+// hand-off that is not an mbarrier is implied by in-order MMA completion (an
+// MMA that overwrites TMEM columns is issued after the MMAs that read them).
+// All MMAs are M=128, N=128 (or N=D), K=16, each 128-deep GEMM issued as one
+// asm block by an elected lane of a converged MMA warp.
+
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -152,13 +146,6 @@ __device__ __forceinline__ uint64_t mnmajor_desc(const void* tile) {
   return make_smem_desc(smem_u32(tile), kBox, 1024);
 }
 
-// 64 packed bf16-pair registers holding 128 values -> 16 x 16B swizzled smem chunks of one row.
-__device__ __forceinline__ void store_row_sw128(uint8_t* tile, int row, const uint32_t* v) {
-#pragma unroll
-  for (int c = 0; c < 16; ++c) {
-    *reinterpret_cast<uint4*>(tile + (c / 8) * kBox + sw128_offset(row, c % 8)) =
-        make_uint4(v[c * 4 + 0], v[c * 4 + 1], v[c * 4 + 2], v[c * 4 + 3]);
-  }
 }
 
 
