@@ -146,9 +146,6 @@ __device__ __forceinline__ uint64_t mnmajor_desc(const void* tile) {
   return make_smem_desc(smem_u32(tile), kBox, 1024);
 }
 
-}
-
-
 #include "ffa_bwd_dkdv.inc"
 
 // =========================================================================== dQ
