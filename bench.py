@@ -196,6 +196,15 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     wl = WORKLOADS[args.workload]
+    workload = args.workload
+    if args.gpus > 1:
+        # the N>1 arm's workload: the CP config-5 shape (cp_bench), per-rank
+        # tokens x N, block-causal 8192; the CPU sample is bounded either way
+        from paper_2505_13211_b200 import cp_bench
+
+        wl = dict(seqlen=cp_bench.PER_RANK * args.gpus, hq=cp_bench.HQ, hk=cp_bench.HK, d=cp_bench.D,
+                  block=cp_bench.BLOCK)
+        workload = "cp_block_causal_magi1_24b"
     for _ in range(args.warmup):
         cpu_baseline_sample(wl, target_s=2.0)
     vals, samples = [], []
@@ -209,7 +218,7 @@ def run_reference(args) -> None:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": args.workload, **wl, "mask": "block_causal"},
+        "config": {"workload": workload, **wl, "mask": "block_causal"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": "port",
                          "sample": base["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
