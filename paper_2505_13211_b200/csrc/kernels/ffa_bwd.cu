@@ -59,7 +59,6 @@ struct BwdParams {
   const void* dout;
   int32_t grad_f32;
   int32_t accumulate;
-  int32_t experiment;  // diagnostics: 1 = no elementwise work, 2 = no gradient MMAs
   int32_t num_k_tiles, num_q_tiles;
   int32_t lse_tma;      // lse / delta rows fetched by TMA (row stride 16B-aligned)
   long long* trace;     // diagnostics: event log of one CTA (nullptr = off)
@@ -320,7 +319,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         // dQ += dS K : A = dS (TMEM, packed into the dP columns: keys [0,64)
         // at +0, keys [64,128) at +64), B = K [keys, D] MN-major
-        if (p.experiment != 2) umma_gemm_ts_dq_k128(t_dq, t_dp, k_mn0 + gst.index * kStageDesc, idesc_q, t > 0 ? 1u : 0u);
+        umma_gemm_ts_dq_k128(t_dq, t_dp, k_mn0 + gst.index * kStageDesc, idesc_q, t > 0 ? 1u : 0u);
         umma_commit_elect(&bars.k_empty[gst.index]);
         gst.advance<S>();
         if (more) {
@@ -373,14 +372,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars.s_full, t & 1);
         tr.ev(10, t);
         tc_fence_after();
-        if (p.experiment == 1) {
-          tc_fence_before();
-          mbar_arrive(&bars.s_free);
-          mbar_wait(&bars.dp_full, t & 1);
-          tc_fence_before();
-          mbar_arrive(&bars.p_full);
-          continue;
-        }
         float pv[64];
         {
           const int kb = k0 + col0;
@@ -578,10 +569,6 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.dout = grad_out;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
-  {
-    const char* e = std::getenv("MAGI_BWD_EXPERIMENT");
-    prm.experiment = e ? std::atoi(e) : 0;
-  }
   if (head_dim == 128) return launch_bwd_impl<128>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
   if (head_dim == 64) return launch_bwd_impl<64>(prm, num_q_tiles, num_k_tiles, q, k, v, grad_out, parts, stream);
   return cudaErrorInvalidValue;

@@ -1,0 +1,58 @@
+"""Every A/B-selectable kernel variant (INTEGRATION.md "Environment knobs")
+computes the same result as the default within the parity tolerances.
+
+The knobs are read once per process, so each variant runs in its own
+subprocess over the d = 128 masks that exercise the full-tile, masked-tile,
+ragged and multiplicity paths, checked against the CPU oracle with the
+tolerances of test_gpu_ffa_fwd.py / test_gpu_ffa_bwd.py.
+"""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+CHECK = r"""
+import math, sys
+import torch
+sys.path.insert(0, ".")
+from oracle import oracle
+from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward
+from tests.ffa_cases import CASES, err_stats, make_inputs
+for name in ("block_causal_gqa_d128", "causal_unaligned", "varlen_mixed", "overlap_multiplicity",
+             "sliding_window", "cross_lk_gt_lq"):
+    sq, sk, hq, hk, d, qr, kr, ty = CASES[name]
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=3)
+    plan = FFAPlan(qr, kr, ty, sq, sk, d)
+    out, lse = ffa_forward(plan, q, k, v)
+    dq, dk, dv = ffa_backward(plan, q, k, v, out, lse, do, grad_dtype=torch.float32)
+    torch.cuda.synchronize()
+    scale = 1.0 / math.sqrt(d)
+    ro, rl = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale)
+    rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ro, rl, do, qr, kr, ty, scale)
+    _, o_rel = err_stats(out.float().cpu().numpy(), ro)
+    l_abs, _ = err_stats(lse.cpu().numpy(), rl)
+    assert o_rel <= 1e-2 and l_abs <= 1e-3, (name, o_rel, l_abs)
+    for nm, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        _, rel = err_stats(got.float().cpu().numpy(), ref)
+        assert rel <= 3e-2, (name, nm, rel)
+print("variant ok")
+"""
+
+VARIANTS = [("MAGI_FWD_VARIANT", v) for v in ("1", "3", "4", "5", "6", "7", "8", "10", "11", "13", "14", "15")]
+VARIANTS += [("MAGI_BWD_POLY", v) for v in ("2", "3", "4")]
+VARIANTS += [("MAGI_DKV_WARPGROUPS", "2"), ("MAGI_DKV_SCHED", "1"), ("MAGI_DQ_POLY", "0"), ("MAGI_DQ_POLY", "2"),
+             ("MAGI_DQ_POLY", "3")]
+
+
+@pytest.mark.parametrize("knob,value", VARIANTS, ids=[f"{k}={v}" for k, v in VARIANTS])
+def test_variant_matches_oracle(built_lib, cuda, knob, value):
+    env = dict(os.environ, **{knob: value})
+    r = subprocess.run([sys.executable, "-c", CHECK], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "variant ok" in r.stdout, r.stdout[-2000:] + r.stderr[-3000:]
