@@ -385,9 +385,9 @@ __global__ void __launch_bounds__(kThreads, 1)
               tc_fence_before();
               mbar_arrive(&bars.s_free);
             }
-            if (all_in) {
-              // x = s * scale * log2e - lse * log2e, two lanes per FFMA2; a
-              // quarter of the exponentials on the FMA pipe
+            {
+              // x = s * scale * log2e - lse * log2e, two lanes per FFMA2; part
+              // of the exponentials on the FMA pipe
               const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
 #pragma unroll
               for (int c = 0; c < 32; c += 2) {
@@ -402,16 +402,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                   pv[h2 * 32 + c + 1] = fast_exp2(x.y);
                 }
               }
-            } else {
-              // packed arithmetic, all exponentials on MUFU, masked keys selected to zero
-              const uint64_t sc2 = f2(sl2, sl2), nl2 = f2(-lse_l2, -lse_l2);
+            }
+            if (!all_in) {
+              // masked keys (and every key of an empty row) selected to exact zeros
 #pragma unroll
-              for (int c = 0; c < 32; c += 2) {
-                const float2 x = f2_split(ffma2(f2(__uint_as_float(s[c]), __uint_as_float(s[c + 1])), sc2, nl2));
+              for (int c = 0; c < 32; ++c) {
                 const int kk = kb + h2 * 32 + c;
-                const float e0 = fast_exp2(x.x), e1 = fast_exp2(x.y);
-                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? e0 : 0.f;
-                pv[h2 * 32 + c + 1] = (kk + 1 >= lo && kk + 1 < hi) ? e1 : 0.f;
+                pv[h2 * 32 + c] = (kk >= lo && kk < hi) ? pv[h2 * 32 + c] : 0.f;
               }
             }
           }
