@@ -260,6 +260,21 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
     tr.ev(13, tkey);
     return;
   }
+  // O rescale (rare: the row max grew by more than 2^8) before the
+  // exponentials, so they and the P stores form one straight-line block; O
+  // is quiescent here (S(t) done implies P(t-1) V done) and the MMA reads it
+  // only after p_full
+  if (t > 0 && __any_sync(0xffffffffu, move)) {
+#pragma unroll 1
+    for (int c = 0; c < OW / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(t_o + oc0 + c * 32, o);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+      tmem_st32(t_o + oc0 + c * 32, o);
+    }
+  }
   uint32_t pk[CW / 2];
   float rs;
   if (full) {
@@ -311,17 +326,6 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
     tmem_st32(t_s + c0, pk);
   } else {
     tmem_st16(t_s + c0, pk);
-  }
-  if (t > 0 && __any_sync(0xffffffffu, move)) {
-#pragma unroll 1
-    for (int c = 0; c < OW / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(t_o + oc0 + c * 32, o);
-      tmem_ld_wait();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-      tmem_st32(t_o + oc0 + c * 32, o);
-    }
   }
   tmem_st_wait();
   tc_fence_before();
