@@ -12,6 +12,7 @@ from __future__ import annotations
 import json
 import os
 import statistics
+import sys
 from pathlib import Path
 
 import torch
@@ -51,6 +52,12 @@ def run(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    # the bench's stdout is one JSON line: native libraries (NCCL prints its
+    # version banner at communicator init) write to fd 1 only as stderr; the
+    # JSON line goes to the saved stdout descriptor
+    sys.stdout.flush()
+    json_fd = os.dup(1)
+    os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=dev)
     ring = getattr(args, "cp_mode", "magi") == "ring"
     if ring:
@@ -195,6 +202,6 @@ def run(args) -> None:
             "clocks": clk,
             "gpu_launches": n_launch * args.steps,
         }
-        print(json.dumps(line), flush=True)
+        os.write(json_fd, (json.dumps(line) + "\n").encode())
     dist.barrier()
     dist.destroy_process_group()
