@@ -87,38 +87,76 @@ __global__ void cast_tail_kernel(const float* __restrict__ src, __nv_bfloat16* _
   if (i < n) dst[i] = __float2bfloat16_rn(src[i]);
 }
 
-// One warp per (row, head): D elements, lanes stride by 8 (bf16) / 4 (f32).
+// delta[h, row] = sum_d dO[row, h, d] * O[row, h, d]. A (row, head) item is
+// D*2 bytes of dO: D/8 lanes read it as 16-byte vectors (O likewise, f32 O as
+// two vectors), so a warp covers 32/(D/8) items per pass and issues kUnroll
+// passes' loads before reducing (HBM-bound: keep bytes in flight).
 template <int D, bool kF32>
 __global__ void bwd_preprocess_kernel(const void* __restrict__ out,
                                       const __nv_bfloat16* __restrict__ dout,
                                       float* __restrict__ delta, int64_t seqlen, int64_t heads) {
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  constexpr int kLanes = D / 8;            // lanes per item
+  constexpr int kPerPass = 32 / kLanes;    // items per warp and pass
+  constexpr int kUnroll = 4;
   const int lane = threadIdx.x % 32;
-  for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
-       w < seqlen * heads; w += warps) {
-    const int64_t row = w / heads, h = w % heads;
-    const int64_t base = w * D;  // [row, head, D] is row-major: (row*heads + h)*D
-    float acc = 0.f;
-    for (int d = lane * 4; d < D; d += 128) {
-      const uint2 g = *reinterpret_cast<const uint2*>(dout + base + d);
-      const __nv_bfloat162 g01 = *reinterpret_cast<const __nv_bfloat162*>(&g.x);
-      const __nv_bfloat162 g23 = *reinterpret_cast<const __nv_bfloat162*>(&g.y);
-      float o0, o1, o2, o3;
-      if constexpr (kF32) {
-        const float4 o = *reinterpret_cast<const float4*>(static_cast<const float*>(out) + base + d);
-        o0 = o.x; o1 = o.y; o2 = o.z; o3 = o.w;
+  const int sub = lane / kLanes, l = lane % kLanes;
+  const int64_t total = seqlen * heads;
+  const int64_t step = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32) * kPerPass * kUnroll;
+  for (int64_t base = (blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32) * kPerPass * kUnroll;
+       base < total; base += step) {
+    uint4 gv[kUnroll];
+    float o[kUnroll][8];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t item = base + u * kPerPass + sub;
+      const int64_t off = item * D + l * 8;  // [row, head, D] row-major: item = row*heads + h
+      if (item < total) {
+        gv[u] = *reinterpret_cast<const uint4*>(dout + off);
+        if constexpr (kF32) {
+          const float4 a = *reinterpret_cast<const float4*>(static_cast<const float*>(out) + off);
+          const float4 b = *reinterpret_cast<const float4*>(static_cast<const float*>(out) + off + 4);
+          o[u][0] = a.x; o[u][1] = a.y; o[u][2] = a.z; o[u][3] = a.w;
+          o[u][4] = b.x; o[u][5] = b.y; o[u][6] = b.z; o[u][7] = b.w;
+        } else {
+          const uint4 ov = *reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(out) + off);
+          const uint32_t w[4] = {ov.x, ov.y, ov.z, ov.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+            o[u][2 * j] = f.x;
+            o[u][2 * j + 1] = f.y;
+          }
+        }
       } else {
-        const uint2 ov = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(out) + base + d);
-        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ov.x));
-        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&ov.y));
-        o0 = a.x; o1 = a.y; o2 = b.x; o3 = b.y;
+        gv[u] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[u][j] = 0.f;
       }
-      const float2 ga = __bfloat1622float2(g01), gb = __bfloat1622float2(g23);
-      acc += o0 * ga.x + o1 * ga.y + o2 * gb.x + o3 * gb.y;
+    }
+    float acc[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint32_t w[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 g = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[j]));
+        a += o[u][2 * j] * g.x + o[u][2 * j + 1] * g.y;
+      }
+      acc[u] = a;
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (lane == 0) delta[h * seqlen + row] = acc;
+    for (int u = 0; u < kUnroll; ++u) {
+#pragma unroll
+      for (int sh = kLanes / 2; sh > 0; sh >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], sh);
+    }
+    if (l == 0) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t item = base + u * kPerPass + sub;
+        if (item < total) delta[(item % heads) * seqlen + item / heads] = acc[u];
+      }
+    }
   }
 }
 
@@ -164,7 +202,7 @@ cudaError_t launch_ffa_bwd_preprocess(const void* out, const void* grad_out, flo
                                       int64_t seqlen, int64_t heads, int head_dim, int out_f32,
                                       cudaStream_t stream) {
   if (seqlen == 0) return cudaSuccess;
-  const int grid = grid_for(seqlen * heads * 32, 256);
+  const int grid = grid_for(seqlen * heads * (head_dim / 8) / 4, 256);
   const auto* g = static_cast<const __nv_bfloat16*>(grad_out);
   if (head_dim == 128) {
     if (out_f32) bwd_preprocess_kernel<128, true><<<grid, 256, 0, stream>>>(out, g, delta, seqlen, heads);
