@@ -63,15 +63,17 @@ constexpr uint32_t kSoftmaxRegs = 104;  // layout 1
 constexpr uint32_t kControlRegs = 56;
 template <int LAYOUT>
 struct FwdLayout {
-  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6;
-  static constexpr bool kSetmaxnreg = LAYOUT == 1 || LAYOUT == 5 || LAYOUT == 6;
+  static constexpr bool kFull5 = LAYOUT == 5 || LAYOUT == 6 || LAYOUT == 7;  // layout 5 family
+  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || kFull5;
+  static constexpr bool kSetmaxnreg = LAYOUT == 1 || kFull5;
   static constexpr bool kSplitP = LAYOUT == 6;  // layout 5 + P handed to the MMA in two key halves
-  static constexpr uint32_t kSoftRegs = (LAYOUT == 5 || LAYOUT == 6) ? 200 : kSoftmaxRegs;
-  static constexpr uint32_t kCtrlRegs = (LAYOUT == 5 || LAYOUT == 6) ? 96 : kControlRegs;
-  static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6) ? 1 : 2);
+  static constexpr bool kToken = LAYOUT == 7;   // layout 5 + exponential loops of the two sub-tiles never overlap
+  static constexpr uint32_t kSoftRegs = kFull5 ? 200 : kSoftmaxRegs;
+  static constexpr uint32_t kCtrlRegs = kFull5 ? 96 : kControlRegs;
+  static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || kFull5) ? 1 : 2);
   static constexpr int kThreads =
-      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : ((LAYOUT == 5 || LAYOUT == 6) ? 384 : 576));
-  static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || LAYOUT == 5 || LAYOUT == 6) ? 8 : 16;
+      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : (kFull5 ? 384 : 576));
+  static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || kFull5) ? 8 : 16;
   static constexpr int kMmaWarp = kTmaWarp + 1;
 };
 constexpr float kLog2e = 1.4426950408889634f;
@@ -115,6 +117,7 @@ struct FwdBarriers {
   uint64_t v_full[kStages], v_empty[kStages];
   uint64_t s_full[2], p_full[2], o_final[2];
   uint64_t p_first[2];  // split P hand-off: keys [0,64) of P stored (layout 6)
+  uint64_t tok[2];      // layout 7: sub-tile i finished the exponentials of a phase
 };
 
 // S = Q K^T (SS, both K-major): descriptors of the two tiles' first k-step;
@@ -154,12 +157,13 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint6
 // [c0, c0 + CW) (CW = 128 / NP, part `part`) of key tile t (global keys from
 // kc), against the row's running (m, l). The NP parts exchange partial maxima
 // through the shared-memory slots at xslot and a named barrier.
-template <int D, int V, int NP, class TRC, bool SPLITP = false>
+template <int D, int V, int NP, class TRC, bool SPLITP = false, bool TOK = false>
 __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int part,
                                               int kc, int lo, int hi, int t, uint32_t xslot,
                                               uint32_t bar_id, float sl2, uint64_t* s_full,
                                               uint64_t* p_full, TRC& tr, int tkey,
-                                              uint64_t* p_first = nullptr) {
+                                              uint64_t* p_first = nullptr, uint64_t* tok_wait = nullptr,
+                                              int tok_parity = -1, uint64_t* tok_arrive = nullptr) {
   constexpr int CW = 128 / NP;
   constexpr int OW = D / NP;  // output columns of this part (O rescale)
   const int c0 = part * CW;
@@ -275,6 +279,11 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
       tmem_st32(t_o + oc0 + c * 32, o);
     }
   }
+  // TOK: the two sub-tiles' exponential loops take turns on the SM
+  // sub-partitions' MUFU pipes instead of slowing each other down
+  if constexpr (TOK) {
+    if (tok_parity >= 0) mbar_wait(tok_wait, static_cast<uint32_t>(tok_parity));
+  }
   uint32_t pk[CW / 2];
   float rs;
   if (full) {
@@ -317,6 +326,7 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
     rs = a2.x + a2.y;
   }
   l = l * alpha + rs;
+  if constexpr (TOK) mbar_arrive(tok_arrive);
   tr.ev(12, tkey);
   // P (bf16 pairs) into the first CW/2 of this part's own (consumed) S columns
   if constexpr (CW == 128) {
@@ -458,6 +468,7 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
       mbar_init(&bars.p_full[i], NP * kSub);
       mbar_init(&bars.p_first[i], NP * kSub);
       mbar_init(&bars.o_final[i], 1);
+      mbar_init(&bars.tok[i], 128);
     }
     fence_barrier_init();
   }
@@ -648,10 +659,13 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
           // slot [t parity][sub][part][row]: a part can run one step ahead of
           // the others' reads, never two
           const uint32_t xslot = xch_base + ((((t & 1) * 2 + sub) * 4) * kSub + row) * 4;
-          softmax_phase<D, V, NP, TracerT<TR>, FwdLayout<LAYOUT>::kSplitP>(
+          // layout 7 turn order: sub-tile 0 phase t after sub-tile 1 phase t-1,
+          // sub-tile 1 phase t after sub-tile 0 phase t
+          const int tok_parity = sub == 0 ? (t > 0 ? ((t - 1) & 1) : -1) : (t & 1);
+          softmax_phase<D, V, NP, TracerT<TR>, FwdLayout<LAYOUT>::kSplitP, FwdLayout<LAYOUT>::kToken>(
               m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off, part, kc, lo[u], hi[u], t,
               xslot, PAIR ? 1 + sub : bar_n, sl2, &bars.s_full[sub], &bars.p_full[sub], tr, kSubs * t + u,
-              &bars.p_first[sub]);
+              &bars.p_first[sub], &bars.tok[sub ^ 1], tok_parity, &bars.tok[sub]);
         }
       }
     }
@@ -698,7 +712,7 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
       cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err != cudaSuccess) return err;
   const dim3 grid(static_cast<unsigned>(prm.num_tiles) * prm.hq);
-  if constexpr (V == 0 && LAYOUT == 5) {
+  if constexpr (V == 0 && (LAYOUT == 5 || LAYOUT == 7)) {
     if (prm.trace != nullptr) {  // diagnostics: the traced instantiation of the default kernel
       err = cudaFuncSetAttribute(ffa_fwd_kernel<D, V, LAYOUT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  smem);
@@ -757,6 +771,8 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
       case 12: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
       case 13: return launch_fwd_impl<128, 1, 5>(prm, q, k, v, stream);
       case 15: return launch_fwd_impl<128, 0, 6>(prm, q, k, v, stream);
+      case 16: return launch_fwd_impl<128, 0, 7>(prm, q, k, v, stream);
+      case 17: return launch_fwd_impl<128, 1, 7>(prm, q, k, v, stream);
       case 14: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
       default: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
     }
