@@ -14,12 +14,19 @@
 using namespace magi;
 
 constexpr int kIters = 512;
-constexpr int NC = 64;
+#ifndef SM_NC
+#define SM_NC 64
+#endif
+#ifndef SM_THREADS
+#define SM_THREADS 256
+#endif
+constexpr int NC = SM_NC;  // columns per thread
+constexpr int kThreadsPerCta = SM_THREADS;  // 256: 2 warps per SMSP; 128: 1
 
 // MASK: pairs (j % 8) computed with the FMA-pipe polynomial.
 // ORDER 0: fused per pair (kernel); 1: all x first, then exps, then sums/packs
 template <uint32_t MASK, int ORDER, bool MAX>
-__global__ void __launch_bounds__(256, 1) k(float* out, long long* clk, float seed) {
+__global__ void __launch_bounds__(kThreadsPerCta, 1) k(float* out, long long* clk, float seed) {
   uint32_t s[NC];
 #pragma unroll
   for (int i = 0; i < NC; ++i) s[i] = __float_as_uint(seed * ((i * 37 + threadIdx.x) % 101) * 0.01f);
@@ -115,13 +122,13 @@ __global__ void __launch_bounds__(256, 1) k(float* out, long long* clk, float se
 
 template <uint32_t MASK, int ORDER, bool MAX>
 void run(const char* name, float* out, long long* clk) {
-  k<MASK, ORDER, MAX><<<148, 256>>>(out, clk, 1.0f);
+  k<MASK, ORDER, MAX><<<148, kThreadsPerCta>>>(out, clk, 1.0f);
   cudaDeviceSynchronize();
   long long c;
   cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
-  const int mufu = 2 * (NC - 2 * __builtin_popcount(MASK) * NC / 16);
-  printf("%-40s %5.0f clk per phase (2 warps x %d columns per SMSP; MUFU bound %d)\n", name,
-         static_cast<double>(c) / kIters, NC, mufu * 8);
+  const int mufu = NC - 2 * __builtin_popcount(MASK) * NC / 16;  // per warp
+  printf("%-40s %5.0f clk per phase (%d warps x %d columns per SMSP; MUFU bound %d)\n", name,
+         static_cast<double>(c) / kIters, kThreadsPerCta / 128, NC, mufu * kThreadsPerCta / 128 * 8);
 }
 
 int main() {
