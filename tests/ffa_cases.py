@@ -36,6 +36,19 @@ CASES = {
                        [FULL, CAUSAL]),
     "causal_lq_gt_lk": (400, 300, 1, 1, 64, [[0, 400]], [[0, 300]], [CAUSAL]),
     "sliding_window": (640, 640, 2, 1, 128, [[0, 96], [96, 640]], [[0, 96], [1, 640]], [CAUSAL, BI]),
+    # keys [0,128), [300,400), [450,512) in no slice: dK/dV must come back 0
+    "uncovered_keys": (256, 512, 2, 1, 128, [[0, 256], [0, 100]], [[128, 300], [400, 450]],
+                       [FULL, CAUSAL]),
+    # zero-length q or k ranges next to real slices (legal: qs <= qe, ks <= ke)
+    "degenerate_slices": (300, 300, 2, 2, 128, [[50, 50], [0, 300], [10, 200]],
+                          [[0, 300], [0, 300], [77, 77]], [FULL, CAUSAL, BI]),
+    # an empty slice list: every row empty, every gradient 0
+    "no_slices": (192, 192, 1, 1, 128, [], [], []),
+    # 41 short documents (1..31 tokens) in one packed sequence, GQA 4:1
+    "many_tiny_docs": (641, 641, 4, 1, 128,
+                       *varlen([1 + (7 * i) % 31 for i in range(41)], [i % 2 for i in range(41)])),
+    # GQA 6:1 at head_dim 64, unaligned causal
+    "gqa6_causal_d64": (333, 333, 6, 1, 64, [[0, 333]], [[0, 333]], [CAUSAL]),
 }
 
 
