@@ -5,7 +5,7 @@
    over its receive buffer, mapped back to global coordinates, equal the
    rank's rows of the global mask pair-for-pair with multiplicity.
 2. The GroupCast / GroupReduce exchange pattern built from it moves exactly
-   the right tokens, run with the gloo backend at world size 2 and 4 (the
+   the right tokens, run with the gloo backend at world size 2, 4 and 8 (the
    NCCL path on GPUs uses the same layouts).
 """
 import json
@@ -30,6 +30,8 @@ MASKS = [
         {"q": [0, 100], "k": [0, 160], "type": "inv_causal"},
         {"q": [40, 160], "k": [10, 150], "type": "bi_causal"},
         {"q": [0, 160], "k": [30, 90], "type": "causal"}]}, 4, 5),
+    # cp 8 (the 1M-token bench shape, scaled down): 64 chunks, 8 per rank
+    ({"seqlen": 512, "pattern": "block_causal", "params": {"block_size": 64}}, 8, 8),
 ]
 
 
@@ -122,7 +124,7 @@ def _exchange_worker(rank, world, port, mask, chunk, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_groupcast_groupreduce_exchange_gloo(built_lib, world):
     mask = {"seqlen": 512, "pattern": "varlen_block_causal", "params": {"sample_lengths": [256, 256],
                                                                         "block_size": 32}}
@@ -144,7 +146,7 @@ def test_groupcast_groupreduce_exchange_gloo(built_lib, world):
     {"seqlen": 4096, "pattern": "varlen_block_causal_last_global",
      "params": {"sample_lengths": [2048, 1024, 1024], "block_size": 512}},
 ])
-@pytest.mark.parametrize("cp", [2, 4])
+@pytest.mark.parametrize("cp", [2, 4, 8])
 def test_ring_plan_covers_mask(built_lib, mask, cp):
     """Ring-attention baseline work lists (zigzag chunks x source rank) cover
     the mask's MULTIPLICITY area exactly, and stay inside the local buffers."""
