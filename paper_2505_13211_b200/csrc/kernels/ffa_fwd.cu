@@ -64,15 +64,17 @@ constexpr uint32_t kControlRegs = 56;
 template <int LAYOUT>
 struct FwdLayout {
   static constexpr bool kFull5 = LAYOUT == 5 || LAYOUT == 6 || LAYOUT == 7;  // layout 5 family
-  static constexpr bool kPair = LAYOUT == 1 || LAYOUT == 4 || kFull5;
-  static constexpr bool kSetmaxnreg = LAYOUT == 1 || kFull5;
+  static constexpr bool kL1 = LAYOUT == 1 || LAYOUT == 8;                    // layout 1 family
+  static constexpr bool kPair = kL1 || LAYOUT == 4 || kFull5;
+  static constexpr bool kSetmaxnreg = kL1 || kFull5;
   static constexpr bool kSplitP = LAYOUT == 6;  // layout 5 + P handed to the MMA in two key halves
   static constexpr bool kToken = LAYOUT == 7;   // layout 5 + exponential loops of the two sub-tiles never overlap
+  static constexpr bool kSpec = LAYOUT == 8;    // layout 1 + exponentials before the row-max exchange
   static constexpr uint32_t kSoftRegs = kFull5 ? 200 : kSoftmaxRegs;
   static constexpr uint32_t kCtrlRegs = kFull5 ? 96 : kControlRegs;
   static constexpr int kParts = LAYOUT == 2 ? 4 : ((LAYOUT == 4 || kFull5) ? 1 : 2);
   static constexpr int kThreads =
-      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (LAYOUT == 1 ? 640 : (kFull5 ? 384 : 576));
+      (LAYOUT == 0 || LAYOUT == 4) ? 320 : (kL1 ? 640 : (kFull5 ? 384 : 576));
   static constexpr int kTmaWarp = (LAYOUT == 0 || LAYOUT == 4 || kFull5) ? 8 : 16;
   static constexpr int kMmaWarp = kTmaWarp + 1;
 };
@@ -157,7 +159,7 @@ __device__ __forceinline__ void issue_pv(uint32_t tmem_o, uint32_t tmem_p, uint6
 // [c0, c0 + CW) (CW = 128 / NP, part `part`) of key tile t (global keys from
 // kc), against the row's running (m, l). The NP parts exchange partial maxima
 // through the shared-memory slots at xslot and a named barrier.
-template <int D, int V, int NP, class TRC, bool SPLITP = false, bool TOK = false>
+template <int D, int V, int NP, class TRC, bool SPLITP = false, bool TOK = false, bool SPEC = false>
 __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, uint32_t t_o, int part,
                                               int kc, int lo, int hi, int t, uint32_t xslot,
                                               uint32_t bar_id, float sl2, uint64_t* s_full,
@@ -182,6 +184,65 @@ __device__ __forceinline__ void softmax_phase(float& m, float& l, uint32_t t_s, 
     for (int i = 0; i < CW; ++i) {
       const int c = kc + i;
       if (c < lo || c >= hi) s[i] = __float_as_uint(-INFINITY);
+    }
+  }
+  if constexpr (SPEC) {
+    // Speculative phase (layout 8): with no masked column and a finite
+    // running max, the exponentials are taken against the current m while the
+    // partial row max is reduced alongside; the parts exchange their maxima
+    // only afterwards. When no row of the warp moves its max, these are the
+    // values the exact phase below would produce (alpha = 1, same m); the two
+    // parts of a row reach the same verdict from the same maxima. Otherwise S
+    // is reloaded from TMEM (P is not stored yet) and both parts redo the
+    // tile exactly.
+    static_assert(NP == 2 && !SPLITP, "speculation is written for the two-part layout");
+    if (__all_sync(0xffffffffu, full && m != -INFINITY)) {
+      const uint64_t sc2 = f2(sl2, sl2), nm2 = f2(-m, -m);
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      uint32_t pk[CW / 2];
+#pragma unroll
+      for (int i = 0; i < CW; i += 2) {
+        const int jj = i / 2;
+        const float s0 = __uint_as_float(s[i]), s1 = __uint_as_float(s[i + 1]);
+        mx[jj % 4] = fmaxf(mx[jj % 4], fmaxf(s0, s1));
+        const float2 x = f2_split(ffma2(f2(s0, s1), sc2, nm2));
+        constexpr uint32_t kPolyMask = V == 0 ? 0x88u : (V == 1 ? 0x92u : 0x80u);
+        float p0, p1;
+        if ((kPolyMask >> (jj % 8)) & 1u) {
+          const float2 e = exp2_poly2(x.x, x.y);
+          p0 = e.x;
+          p1 = e.y;
+        } else {
+          p0 = fast_exp2(x.x);
+          p1 = fast_exp2(x.y);
+        }
+        acc2[jj % 4] = fadd2(acc2[jj % 4], f2(p0, p1));
+        pk[jj] = pack_bf16(p0, p1);
+      }
+      float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+      asm volatile("st.shared.f32 [%0], %1;" ::"r"(xslot + part * kSub * 4), "f"(mt) : "memory");
+      named_bar_sync(bar_id, NP * 128);
+#pragma unroll
+      for (int o = 1; o < NP; ++o) {
+        float po;
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(po) : "r"(xslot + ((part + o) % NP) * kSub * 4) : "memory");
+        mt = fmaxf(mt, po);
+      }
+      if (!__any_sync(0xffffffffu, mt * sl2 > m + kRescaleThreshold)) {
+        const float2 a2 = f2_split(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])));
+        l = l + (a2.x + a2.y);
+        tr.ev(12, tkey);
+        tmem_st32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(p_full);
+        tr.ev(13, tkey);
+        return;
+      }
+#pragma unroll
+      for (int c = 0; c < CW / 32; ++c) tmem_ld32(t_s + c0 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
+      tmem_ld_wait();
     }
   }
   // partial row max as 4 independent 3-input-max chains
@@ -662,7 +723,8 @@ __global__ void __launch_bounds__(FwdLayout<LAYOUT>::kThreads, 1)
           // layout 7 turn order: sub-tile 0 phase t after sub-tile 1 phase t-1,
           // sub-tile 1 phase t after sub-tile 0 phase t
           const int tok_parity = sub == 0 ? (t > 0 ? ((t - 1) & 1) : -1) : (t & 1);
-          softmax_phase<D, V, NP, TracerT<TR>, FwdLayout<LAYOUT>::kSplitP, FwdLayout<LAYOUT>::kToken>(
+          softmax_phase<D, V, NP, TracerT<TR>, FwdLayout<LAYOUT>::kSplitP, FwdLayout<LAYOUT>::kToken,
+                        FwdLayout<LAYOUT>::kSpec>(
               m[u], l[u], tmem + sub * 128 + lane_off, tmem + 256 + sub * 128 + lane_off, part, kc, lo[u], hi[u], t,
               xslot, PAIR ? 1 + sub : bar_n, sl2, &bars.s_full[sub], &bars.p_full[sub], tr, kSubs * t + u,
               &bars.p_first[sub], &bars.tok[sub ^ 1], tok_parity, &bars.tok[sub]);
@@ -773,6 +835,8 @@ cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_t
       case 15: return launch_fwd_impl<128, 0, 6>(prm, q, k, v, stream);
       case 16: return launch_fwd_impl<128, 0, 7>(prm, q, k, v, stream);
       case 17: return launch_fwd_impl<128, 1, 7>(prm, q, k, v, stream);
+      case 18: return launch_fwd_impl<128, 0, 8>(prm, q, k, v, stream);
+      case 19: return launch_fwd_impl<128, 1, 8>(prm, q, k, v, stream);
       case 14: return launch_fwd_impl<128, 1, 0>(prm, q, k, v, stream);
       default: return launch_fwd_impl<128, 0, 5>(prm, q, k, v, stream);
     }

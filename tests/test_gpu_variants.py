@@ -44,7 +44,7 @@ for name in ("block_causal_gqa_d128", "causal_unaligned", "varlen_mixed", "overl
 print("variant ok")
 """
 
-VARIANTS = [("MAGI_FWD_VARIANT", v) for v in ("1", "3", "4", "5", "6", "7", "8", "10", "11", "13", "14", "15", "16", "17")]
+VARIANTS = [("MAGI_FWD_VARIANT", v) for v in ("1", "3", "4", "5", "6", "7", "8", "10", "11", "13", "14", "15", "16", "17", "18", "19")]
 VARIANTS += [("MAGI_BWD_POLY", v) for v in ("2", "3", "4")]
 VARIANTS += [("MAGI_DKV_WARPGROUPS", "2"), ("MAGI_DKV_SCHED", "1"), ("MAGI_DQ_POLY", "0"), ("MAGI_DQ_POLY", "2"),
              ("MAGI_DQ_POLY", "3")]

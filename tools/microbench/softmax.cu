@@ -25,7 +25,7 @@ constexpr int kThreadsPerCta = SM_THREADS;  // 256: 2 warps per SMSP; 128: 1
 
 // MASK: pairs (j % 8) computed with the FMA-pipe polynomial.
 // ORDER 0: fused per pair (kernel); 1: all x first, then exps, then sums/packs
-template <uint32_t MASK, int ORDER, bool MAX>
+template <uint32_t MASK, int ORDER, bool MAX, bool SUM = true>
 __global__ void __launch_bounds__(kThreadsPerCta, 1) k(float* out, long long* clk, float seed) {
   uint32_t s[NC];
 #pragma unroll
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreadsPerCta, 1) k(float* out, long long* cl
           p0 = fast_exp2(x.x);
           p1 = fast_exp2(x.y);
         }
-        acc2[j % 4] = fadd2(acc2[j % 4], f2(p0, p1));
+        if (SUM) acc2[j % 4] = fadd2(acc2[j % 4], f2(p0, p1));
         pk[j] = pack_bf16(p0, p1);
       }
     } else {
@@ -120,9 +120,9 @@ __global__ void __launch_bounds__(kThreadsPerCta, 1) k(float* out, long long* cl
   if (threadIdx.x == 0) clk[blockIdx.x] = c1 - c0;
 }
 
-template <uint32_t MASK, int ORDER, bool MAX>
+template <uint32_t MASK, int ORDER, bool MAX, bool SUM = true>
 void run(const char* name, float* out, long long* clk) {
-  k<MASK, ORDER, MAX><<<148, kThreadsPerCta>>>(out, clk, 1.0f);
+  k<MASK, ORDER, MAX, SUM><<<148, kThreadsPerCta>>>(out, clk, 1.0f);
   cudaDeviceSynchronize();
   long long c;
   cudaMemcpy(&c, clk, 8, cudaMemcpyDeviceToHost);
@@ -144,6 +144,9 @@ int main() {
   run<0x88u, 1, true>("25% poly, staged", out, clk);
   run<0x92u, 1, true>("37.5% poly, staged", out, clk);
   run<0x88u, 0, false>("25% poly, fused, no max", out, clk);
+  run<0x88u, 0, true, false>("25% poly, fused, no row sum", out, clk);
+  run<0x92u, 0, true, false>("37.5% poly, fused, no row sum", out, clk);
+  run<0x88u, 0, false, false>("25% poly, fused, no max, no sum", out, clk);
   printf("status %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
