@@ -80,6 +80,16 @@ static std::string capi_simulate(const std::string& scenario) {
   return res;
 }
 
+static std::string capi_pack(const std::string& config, const char* stream) {
+  char* out = nullptr;
+  if (magiplan_pack_run(config.c_str(), stream, &out) != MAGIPLAN_OK) {
+    return std::string("ERROR ") + magiplan_last_error();
+  }
+  std::string res(out);
+  magiplan_string_free(out);
+  return res;
+}
+
 int main(int argc, char** argv) {
   const std::string path = argc > 1 ? argv[1] : "ref_planner.json";
   std::mt19937_64 rng(20250519);
@@ -333,6 +343,45 @@ int main(int argc, char** argv) {
                                  R"(, "sweep": {"cp_sizes": [1, 2, 4, 8], "per_rank_seqlen": 8192})");
   sc.push_back({{"scenario", sweep}, {"simulate", capi_simulate(sweep)}});
   g["scenarios"] = sc;
+
+  // ---- packer runs through the reference C ABI (pack.cpp, scenario.cpp:428-554)
+  json pk_runs = json::array();
+  std::vector<std::string> pack_cfgs = {
+      R"({"packing": {"max_length": 65536, "bins_per_iteration": 8, "pool_capacity": 64, "dp_size": 4, "cp_size": 8}, "generator": {"count": 2000, "median": 8192, "sigma": 1.0}, "seed": 3})",
+      R"({"packing": {"max_length": 32768, "bins_per_iteration": 2, "pool_capacity": 8}, "generator": {"count": 300, "median": 2048, "sigma": 1.0}, "seed": 42, "emit_bins": true})",
+      R"({"packing": {"max_length": 16384, "bins_per_iteration": 4, "pool_capacity": 16, "swap_passes": 0, "defer_threshold": 0.9}, "generator": {"count": 500, "median": 6000, "sigma": 1.5}, "seed": 9})",
+      R"({"packing": {"max_length": 4096, "bins_per_iteration": 3, "pool_capacity": 12, "defer_threshold": 1.0}, "generator": {"count": 200, "median": 1500, "sigma": 0.7}, "seed": 5, "emit_bins": true})",
+      R"({"generator": {"count": 50}, "seed": 1})",
+      R"({"packing": {"max_length": 32768, "bins_per_iteration": 2, "pool_capacity": 32}, "generator": {"count": 300, "median": 2048, "sigma": 1.0}, "seed": 42, "emit_bins": true})",
+      R"({"packing": {"max_length": 8192, "bins_per_iteration": 4, "pool_capacity": 16, "dp_size": 2}, "generator": {"count": 400, "median": 3000, "sigma": 2.0}, "seed": 11, "emit_bins": true})",
+      R"({"packing": {"bins_per_iteration": 3, "dp_size": 2, "pool_capacity": 12}, "generator": {}})",
+      R"({"packing": {"max_length": 1000, "tp_size": 3}, "generator": {}})",
+      R"({"packing": {"bins_per_iteration": 4, "pool_capacity": 8}, "generator": {}})",
+      R"({"packing": {"defer_threshold": 1.5}, "generator": {}})",
+      R"({"packing": {"max_length": 0}, "generator": {}})",
+      R"({"packing": {"bogus": 1}})",
+      R"({"generator": {"count": 10, "mean": 3}})",
+      R"({"seed": 1})",
+      R"([1, 2])",
+      R"({"packing": )",
+  };
+  for (const auto& c : pack_cfgs) pk_runs.push_back({{"config", c}, {"out", capi_pack(c, nullptr)}});
+  std::vector<std::pair<std::string, std::string>> pack_streams = {
+      {R"({"packing": {"max_length": 100, "bins_per_iteration": 2, "pool_capacity": 8}, "emit_bins": true})",
+       "# id length\n0 60\n1 50\n2 40\n\n3 30\n4 200\n5 0\n6 45\n7 55\n8 10\n9 90\n10 35\n11 65\n12 5\n"},
+      {R"({"packing": {"max_length": 100, "bins_per_iteration": 4, "pool_capacity": 16, "defer_threshold": 0.0}, "emit_bins": true})",
+       "0 100\n1 1\n2 1\n3 1\n4 1\n5 1\n"},
+      {R"({"packing": {"max_length": 10, "bins_per_iteration": 1, "pool_capacity": 4}})",
+       "0 11\n1 12\n2 13\n3 14\n4 15\n5 16\n6 17\n7 18\n8 19\n9 20\n10 21\n11 22\n12 23\n13 24\n14 25\n15 26\n16 27\n17 28\n18 29\n19 30\n20 31\n21 32\n22 3\n"},
+      {R"({"packing": {"max_length": 100, "bins_per_iteration": 2, "pool_capacity": 8, "defer_threshold": 0.95}})",
+       "0 10\n1 10\n2 10\n3 10\n4 10\n5 10\n6 10\n7 10\n8 10\n9 10\n"},
+      {R"({"packing": {"max_length": 100}})", "0 20\n1 x\n"},
+      {R"({})", ""},
+  };
+  for (const auto& [c, st] : pack_streams) {
+    pk_runs.push_back({{"config", c}, {"stream", st}, {"out", capi_pack(c, st.c_str())}});
+  }
+  g["pack_runs"] = pk_runs;
 
   std::ofstream(path) << g.dump() << "\n";
   std::printf("wrote %s\n", path.c_str());

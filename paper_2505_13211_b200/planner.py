@@ -107,3 +107,31 @@ def debug_eval(op: str, **kwargs: Any):
 def lognormal_lengths(count: int, median: float, sigma: float, max_length: int, seed: int) -> list[int]:
     return debug_eval("lognormal", count=count, median=median, sigma=sigma, max_length=max_length,
                       seed=seed)
+
+
+def pack_run_text(config: dict | str, stream: str | None = None) -> str:
+    """magiplan_pack_run: the online packing-and-padding report (reference
+    proj/src/scenario.cpp:428-554). `stream` holds "id length" lines; None
+    uses the config's log-normal generator."""
+    text = config if isinstance(config, str) else json.dumps(config)
+    out = C.c_void_p()
+    _lib.check(_lib.lib().magiplan_pack_run(text.encode(), None if stream is None else stream.encode(),
+                                            C.byref(out)))
+    return _lib.take_string(out)
+
+
+def pack_run(config: dict | str, stream: str | None = None) -> dict:
+    return json.loads(pack_run_text(config, stream))
+
+
+def pack_samples(lengths: list[int], max_length: int, bins: int, pool_capacity: int | None = None,
+                 **packing: Any) -> list[list[int]]:
+    """Pack a length list with the reference packer and return, per emitted
+    bin, its sample lengths in bin order: the varlen document lists a packed
+    FFA batch (config 4) is built from."""
+    cfg = {"packing": {"max_length": max_length, "bins_per_iteration": bins,
+                       "pool_capacity": pool_capacity or 4 * bins, **packing},
+           "emit_bins": True}
+    stream = "".join(f"{i} {n}\n" for i, n in enumerate(lengths))
+    rep = pack_run(cfg, stream)
+    return [[s["length"] for s in b["samples"]] for batch in rep["batches"] for b in batch["bins"]]

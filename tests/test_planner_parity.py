@@ -117,3 +117,44 @@ def test_scenarios_byte_identical(P, idx):
                 sc.simulate_text(2)
         else:
             assert sc.simulate_text(2) == e["simulate"]
+
+
+@pytest.mark.parametrize("idx", range(len(GOLD["pack_runs"])))
+def test_pack_run_byte_identical(P, idx):
+    """magiplan_pack_run against the reference library's report, byte for
+    byte; errors by class and message (reference capi.cpp:188-198,
+    scenario.cpp:428-554, pack.cpp:30-226)."""
+    from paper_2505_13211_b200 import _lib
+
+    e = GOLD["pack_runs"][idx]
+    if e["out"].startswith("ERROR "):
+        with pytest.raises(_lib.MagiplanError) as ei:
+            P.pack_run_text(e["config"], e.get("stream"))
+        assert ei.value.message == e["out"][len("ERROR "):]
+        kind = _lib.ConstraintError if "constraint violated" in e["out"] else _lib.UsageError
+        assert isinstance(ei.value, kind)
+    else:
+        assert P.pack_run_text(e["config"], e.get("stream")) == e["out"]
+
+
+def test_pack_invariants(P):
+    """Every emitted bin fits max_length and is non-empty, each sample is
+    packed at most once, and the counts balance (reference pack.cpp:135-196)."""
+    lengths = P.lognormal_lengths(3000, 2048.0, 1.0, 32768, 42)
+    cfg = {"packing": {"max_length": 32768, "bins_per_iteration": 8, "pool_capacity": 64, "dp_size": 4},
+           "emit_bins": True}
+    stream = "".join(f"{i} {n}\n" for i, n in enumerate(lengths))
+    rep = P.pack_run(cfg, stream)
+    seen = set()
+    for batch in rep["batches"]:
+        assert len(batch["bins"]) == 8
+        for b in batch["bins"]:
+            assert b["samples"] and b["fill"] == sum(s["length"] for s in b["samples"]) <= 32768
+            for s in b["samples"]:
+                assert s["id"] not in seen and lengths[s["id"]] == s["length"]
+                seen.add(s["id"])
+    assert rep["samples_packed"] == len(seen)
+    assert rep["samples_packed"] + rep["samples_left"] + rep["skipped_oversized"] == rep["samples_in"]
+    assert rep["stats"]["min_utilization"] >= 0.5  # the default defer_threshold
+    docs = P.pack_samples(lengths[:200], 32768, 2)
+    assert all(sum(d) <= 32768 for d in docs)
