@@ -330,6 +330,23 @@ int main(int argc, char** argv) {
                              R"(, "pattern": "block_causal", "params": {"block_size": 8192}})",
                          ", \"cp_size\": " + std::to_string(cp)));
   }
+  // baseline schedules (sim.cpp:262-537)
+  texts.push_back(scen(R"({"seqlen": 16384, "pattern": "block_causal", "params": {"block_size": 2048}})",
+                       R"(, "cp_size": 8, "schedule": "ring")"));
+  texts.push_back(scen(R"({"seqlen": 4096, "pattern": "causal"})", R"(, "cp_size": 4, "schedule": "ring_serial")"));
+  texts.push_back(scen(R"({"seqlen": 3072, "pattern": "sliding_window_causal", "params": {"window": 500}})",
+                       R"(, "cp_size": 3, "schedule": "ring", "dispatch_chunk_size": 128)"));
+  texts.push_back(scen(R"({"seqlen": 32768, "pattern": "block_causal", "params": {"block_size": 4096}})",
+                       R"(, "cp_size": 8, "schedule": "ulysses")"));
+  texts.push_back(scen(R"({"seqlen": 6000, "pattern": "causal"})", R"(, "cp_size": 3, "schedule": "ulysses")"));
+  texts.push_back(scen(R"({"seqlen": 6000, "pattern": "causal"})", R"(, "cp_size": 7, "schedule": "ulysses")"));
+  for (int nc : {2, 3, 5, 8}) {
+    texts.push_back(scen(R"({"seqlen": 32768, "pattern": "block_causal", "params": {"block_size": 4096}})",
+                         ", \"cp_size\": 4, \"schedule\": \"cso\", \"cso_num_chunks\": " + std::to_string(nc)));
+  }
+  texts.push_back(scen(R"({"seqlen": 8192, "pattern": "full"})", R"(, "cp_size": 2, "schedule": "cso", "cso_num_chunks": 1)"));
+  texts.push_back(scen(R"({"seqlen": 8190, "pattern": "full"})", R"(, "cp_size": 4, "schedule": "cso")"));
+  texts.push_back(R"({"workload": {"mask": {"seqlen": 4096, "pattern": "causal"}, "num_heads_q": 24, "num_heads_k": 8, "num_heads_v": 8, "head_dim": 128}, "cp_size": 2, "schedule": "ulysses"})");
   texts.push_back(scen(R"({"seqlen": 8, "pattern": "full"})", R"(, "cp_size": 3)"));  // constraint error
   texts.push_back(R"({"workload": {"mask": {"seqlen": 8, "pattern": "causal"}}, "bogus": 1})");  // usage
   for (const auto& t : texts) {
@@ -342,6 +359,12 @@ int main(int argc, char** argv) {
   const std::string sweep = scen(R"({"seqlen": 8192, "pattern": "full"})",
                                  R"(, "sweep": {"cp_sizes": [1, 2, 4, 8], "per_rank_seqlen": 8192})");
   sc.push_back({{"scenario", sweep}, {"simulate", capi_simulate(sweep)}});
+  for (const char* sched : {"ring", "ulysses", "cso"}) {
+    const std::string sw = scen(R"({"seqlen": 8192, "pattern": "causal"})",
+                                std::string(R"(, "schedule": ")") + sched +
+                                    R"(", "sweep": {"cp_sizes": [1, 2, 4, 8], "per_rank_seqlen": 4096})");
+    sc.push_back({{"scenario", sw}, {"simulate", capi_simulate(sw)}});
+  }
   g["scenarios"] = sc;
 
   // ---- packer runs through the reference C ABI (pack.cpp, scenario.cpp:428-554)

@@ -277,17 +277,25 @@ std::string plan_artifacts_to_json(const PlanArtifacts& a, const ScenarioSpec& s
 namespace {
 
 std::vector<std::string> simulate_point(const ScenarioSpec& spec, Token seqlen) {
-  if (spec.schedule != "magi") {
-    throw UsageError("schedule '" + spec.schedule +
-                     "' is not part of this build: only the magi multi-stage schedule is modelled "
-                     "(ring/ulysses/cso are out of scope, see DESIGN.md)");
-  }
+  // reference scenario.cpp:341-366
   const AttnMask m = scenario_mask(spec, seqlen);
-  const PlanArtifacts a = run_plan(spec, m);
-  auto [fwd, bwd] = simulate_magi(a.mask, a.plan, a.cast_table, a.reduce_table, a.stages,
-                                  spec.cost_model, spec.workload);
+  std::vector<SimReport> reports;
+  if (spec.schedule == "magi") {
+    const PlanArtifacts a = run_plan(spec, m);
+    auto [fwd, bwd] = simulate_magi(a.mask, a.plan, a.cast_table, a.reduce_table, a.stages,
+                                    spec.cost_model, spec.workload);
+    reports = {std::move(fwd), std::move(bwd)};
+  } else if (spec.schedule == "ring" || spec.schedule == "ring_serial") {
+    const PlanArtifacts a = run_plan(spec, m);
+    auto [fwd, bwd] = simulate_ring(a.mask, a.plan, spec.cost_model, spec.workload, spec.schedule == "ring");
+    reports = {std::move(fwd), std::move(bwd)};
+  } else if (spec.schedule == "ulysses") {
+    reports.push_back(simulate_ulysses(m, spec.workload, spec.cost_model, spec.cp_size));
+  } else {
+    reports.push_back(simulate_cso(m, spec.workload, spec.cost_model, spec.cp_size, spec.cso_num_chunks));
+  }
   std::vector<std::string> out;
-  for (const SimReport* r : {&fwd, &bwd}) {
+  for (const SimReport* r = reports.data(); r != reports.data() + reports.size(); ++r) {
     json rec;
     rec["schema_version"] = kSchemaVersion;
     rec["spec_hash"] = spec.spec_hash;

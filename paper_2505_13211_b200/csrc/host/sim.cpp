@@ -77,9 +77,8 @@ Rank Timeline::bottleneck_rank() const {
   return best;
 }
 
-namespace {
-
-SimReport report(std::string schedule, Pass pass, Rank cp, Timeline& tl, int64_t fl, int64_t vol) {
+SimReport finish_report(std::string schedule, Pass pass, Rank cp, Timeline& tl, int64_t fl, int64_t vol,
+                        std::vector<std::string> event_log) {
   tl.run();
   SimReport r;
   r.schedule = std::move(schedule);
@@ -97,10 +96,9 @@ SimReport report(std::string schedule, Pass pass, Rank cp, Timeline& tl, int64_t
   r.flops_total = fl;
   r.throughput_per_gpu = r.makespan > 0 ? throughput(fl, r.makespan, cp) : 0.0;
   r.comm_volume_tokens = vol;
+  r.event_log = std::move(event_log);
   return r;
 }
-
-}  // namespace
 
 std::string sim_report_to_json(const SimReport& r) {
   nlohmann::ordered_json j;
@@ -115,6 +113,7 @@ std::string sim_report_to_json(const SimReport& r) {
   j["flops_total"] = r.flops_total;
   j["throughput_per_gpu"] = r.throughput_per_gpu;
   j["comm_volume_tokens"] = r.comm_volume_tokens;
+  if (!r.event_log.empty()) j["event_log"] = r.event_log;
   return j.dump();
 }
 
@@ -169,8 +168,8 @@ std::pair<SimReport, SimReport> simulate_magi(const AttnMask& m, const DispatchP
             "reduce(" + std::to_string(b.num_stages) + ")");
   }
   const int64_t cv = cast.total_token_transfers(), rv = reduce.total_token_transfers();
-  return {report("magi", Pass::Fwd, cp, fwd, flops(m, w, Pass::Fwd), cv),
-          report("magi", Pass::Bwd, cp, bwd, flops(m, w, Pass::Bwd), cv + rv)};
+  return {finish_report("magi", Pass::Fwd, cp, fwd, flops(m, w, Pass::Fwd), cv),
+          finish_report("magi", Pass::Bwd, cp, bwd, flops(m, w, Pass::Bwd), cv + rv)};
 }
 
 }  // namespace magiplan

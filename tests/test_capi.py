@@ -112,15 +112,35 @@ def test_plan_and_simulate_agree(built_lib):
     assert fwd["makespan"] == est_f and bwd["makespan"] == est_b
 
 
-def test_out_of_scope_entry_points_fail_loudly(built_lib):
+def test_every_schedule_simulates(built_lib):
+    """All five schedules of the reference simulator (sim.cpp:174-537) run
+    through magiplan_scenario_simulate; magi/ring give fwd+bwd records,
+    Ulysses/cso a forward record with its step log; errors map like the
+    reference's (cso chunk count: USAGE, indivisible seqlen: CONSTRAINT)."""
     from paper_2505_13211_b200 import _lib
-
     from paper_2505_13211_b200.planner import Scenario
 
-    sc = Scenario({"workload": {"mask": {"seqlen": 64, "pattern": "causal"}}, "cp_size": 2,
-                   "schedule": "ulysses"})
+    def sim(schedule, seqlen=4096, cp=4, **extra):
+        aff = lambda lat, pu: {"latency": lat, "per_unit": pu}  # noqa: E731
+        cost = {"ffa_fwd": aff(30, 8.19e-05), "ffa_bwd": aff(30, 2.05e-04), "cast": aff(100, 0.082),
+                "reduce": aff(100, 0.082), "q_proj": aff(10, 0.5), "k_proj": aff(10, 0.1),
+                "v_proj": aff(10, 0.1), "kv_cache_update": aff(5, 0.05), "cross_attn": aff(10, 0.3)}
+        spec = {"workload": {"mask": {"seqlen": seqlen, "pattern": "causal"}}, "cp_size": cp,
+                "schedule": schedule, "cost_model": cost, **extra}
+        return [json.loads(l) for l in Scenario(spec).simulate_text().splitlines()]
+
+    for sched, passes in (("magi", ["fwd", "bwd"]), ("ring", ["fwd", "bwd"]),
+                          ("ring_serial", ["fwd", "bwd"]), ("ulysses", ["fwd"]), ("cso", ["fwd"])):
+        recs = sim(sched)
+        assert [r["pass"] for r in recs] == passes and all(r["schedule"] == sched for r in recs)
+        assert all(r["makespan"] > 0 and len(r["per_rank_makespan"]) == 4 for r in recs)
+    # overlapping the ring hops never loses to the serial ring
+    assert sim("ring")[0]["makespan"] <= sim("ring_serial")[0]["makespan"]
+    assert len(sim("cso", cso_num_chunks=3)[0]["event_log"]) == 3 + 3
     with pytest.raises(_lib.UsageError):
-        sc.simulate_text()
+        sim("cso", cso_num_chunks=1)
+    with pytest.raises(_lib.ConstraintError):
+        sim("ulysses", seqlen=4098)
 
 
 def test_ffa_plan_validation_on_cpu(built_lib):
