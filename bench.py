@@ -442,8 +442,9 @@ def main() -> None:
     ap.add_argument("--impl", default="magi", choices=["magi", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cp-mode", default="magi", choices=["magi", "ring"],
-                    help="N>1 only: MagiAttention GroupCast CP (default) or the ring-attention baseline")
+    ap.add_argument("--cp-mode", default="magi", choices=["magi", "ring", "ulysses"],
+                    help="N>1 only: MagiAttention GroupCast CP (default), or the ring-attention / "
+                         "Ulysses all-to-all baselines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -59,11 +59,17 @@ def run(args) -> None:
     json_fd = os.dup(1)
     os.dup2(2, 1)
     dist.init_process_group("nccl", device_id=dev)
-    ring = getattr(args, "cp_mode", "magi") == "ring"
+    mode = getattr(args, "cp_mode", "magi")
+    ring = mode == "ring"
+    uly = mode == "ulysses"
     if ring:
         from paper_2505_13211_b200.ring import RingAttention
 
         cpa = RingAttention(scenario(world)["workload"]["mask"], HQ, HK, D)
+    elif uly:
+        from paper_2505_13211_b200.ulysses import UlyssesAttention
+
+        cpa = UlyssesAttention(scenario(world)["workload"]["mask"], HQ, HK, D)
     else:
         cpa = CPAttention(scenario(world), HQ, HK, D)
     L = cpa.local_tokens
@@ -166,7 +172,9 @@ def run(args) -> None:
         value = total / (ms.item() * 1e-3) / 1e12
         per_gpu = value / world
         n_launch = 0
-        if ring:
+        if uly:
+            n_launch = 1 + 1 + 1 + 3  # fwd, cast, preprocess, dkdv + dq + final casts inside ffa_bwd
+        elif ring:
             n_plans = sum(p is not None for p in cpa.plans)
             n_launch = n_plans * 3 + 1 + 1 + 3  # fwd + dq + dkdv per plan, cast, preprocess, final casts
         else:
@@ -181,11 +189,11 @@ def run(args) -> None:
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": "cp_block_causal_magi1_24b", "seqlen": PER_RANK * world,
                        "tokens_per_rank": PER_RANK, "num_heads_q": HQ, "num_heads_k": HK, "head_dim": D,
-                       "mask": f"block_causal(block={BLOCK})", "dispatch": "zigzag" if ring else "greedy",
-                       "cp_mode": "ring" if ring else "magi",
-                       "dispatch_chunk_size": cpa.chunk_size,
-                       "num_stages_fwd": world if ring else cpa.xplan["num_stages_fwd"],
-                       "num_stages_bwd": world if ring else cpa.xplan["num_stages_bwd"],
+                       "mask": f"block_causal(block={BLOCK})", "dispatch": "zigzag" if ring else ("contiguous" if uly else "greedy"),
+                       "cp_mode": mode,
+                       "dispatch_chunk_size": cpa.local_tokens if uly else cpa.chunk_size,
+                       "num_stages_fwd": world if ring else (1 if uly else cpa.xplan["num_stages_fwd"]),
+                       "num_stages_bwd": world if ring else (1 if uly else cpa.xplan["num_stages_bwd"]),
                        "parallelism": f"cp{world}",
                        "flops_per_step": total,
                        "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),

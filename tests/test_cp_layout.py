@@ -166,3 +166,45 @@ def test_ring_plan_covers_mask(built_lib, mask, cp):
                 assert 0 <= qs < qe <= len(chunks[r]) * cs and 0 <= ks < ke <= len(chunks[s]) * cs
             total += sum(debug_eval("slice_area", slice=x) for x in sl)
     assert total == debug_eval("mask", mask=mask)["area_multiplicity"]
+
+
+def _ulysses_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_13211_b200.ulysses import _heads_to_tokens, _tokens_to_heads
+
+        S, H, d = 8 * world, 2 * world, 3
+        # value = token * 1000 + head * 10 + lane, so every element names its place
+        full = (torch.arange(S)[:, None, None] * 1000 + torch.arange(H)[None, :, None] * 10
+                + torch.arange(d)[None, None, :]).to(torch.float32)
+        L = S // world
+        shard = full[rank * L:(rank + 1) * L].contiguous()
+        hl = H // world
+        heads = _tokens_to_heads(shard, world, None)
+        ok = torch.equal(heads, full[:, rank * hl:(rank + 1) * hl])
+        ok &= torch.equal(_heads_to_tokens(heads, world, None), shard)
+        lse_full = full[:, :, 0].t().contiguous()  # [H, S]
+        lse_h = lse_full[rank * hl:(rank + 1) * hl]  # this rank's heads, every token
+        back = _heads_to_tokens(lse_h.t().contiguous(), world, None).t()
+        ok &= torch.equal(back, lse_full[:, rank * L:(rank + 1) * L])
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ulysses_all_to_all_layout_gloo(world):
+    """Ulysses CP (ulysses.py): token shard -> head shard over the whole
+    sequence and back, and the LSE [heads, tokens] exchange, on gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29650 + world
+    procs = [ctx.Process(target=_ulysses_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res

@@ -24,8 +24,12 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode="magi"):
     try:
         from paper_2505_13211_b200.cp import CPAttention
         from paper_2505_13211_b200.ring import RingAttention
+        from paper_2505_13211_b200.ulysses import UlyssesAttention
 
-        if mode == "ring":
+        if mode == "ulysses":
+            cpa = UlyssesAttention(mask, hq, hk, d)
+            S = cpa.seqlen
+        elif mode == "ring":
             cpa = RingAttention(mask, hq, hk, d)
             S = cpa.chunk_size * 2 * world
         else:
@@ -60,6 +64,10 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode="magi"):
     # ring-attention baseline (zigzag dispatch, K/V around the ring)
     ("ring", {"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 0),
     ("ring", {"seqlen": 4096, "pattern": "causal"}, 0),
+    # Ulysses all-to-all baseline (head-parallel, contiguous token shards)
+    ("ulysses", {"seqlen": 4096, "pattern": "block_causal", "params": {"block_size": 512}}, 0),
+    ("ulysses", {"seqlen": 2048, "pattern": "varlen_block_causal_last_global",
+                 "params": {"sample_lengths": [1024, 512, 512], "block_size": 256}}, 0),
 ])
 def test_cp_matches_oracle(built_lib, cuda, mode, mask, chunk):
     if torch.cuda.device_count() < 2:
@@ -68,10 +76,10 @@ def test_cp_matches_oracle(built_lib, cuda, mode, mask, chunk):
     from paper_2505_13211_b200.planner import Mask
 
     world = min(4, torch.cuda.device_count())
-    hq, hk, d = 4, 2, 128
+    hq, hk, d = (8, 4, 128) if mode == "ulysses" else (4, 2, 128)
     ctx = mp.get_context("spawn")
     qu = ctx.Queue()
-    port = 29700 + chunk % 97 + (37 if mode == "ring" else 0) + (mask["seqlen"] % 89)
+    port = 29700 + chunk % 97 + {"ring": 37, "ulysses": 53}.get(mode, 0) + (mask["seqlen"] % 89)
     ps = [ctx.Process(target=_worker, args=(r, world, port, mask, chunk, hq, hk, d, qu, mode))
           for r in range(world)]
     for p in ps:
