@@ -135,3 +135,21 @@ def pack_samples(lengths: list[int], max_length: int, bins: int, pool_capacity: 
     stream = "".join(f"{i} {n}\n" for i, n in enumerate(lengths))
     rep = pack_run(cfg, stream)
     return [[s["length"] for s in b["samples"]] for batch in rep["batches"] for b in batch["bins"]]
+
+
+def packed_bin_masks(lengths: list[int], max_length: int, bins: int, pool_capacity: int | None = None,
+                     causal_odd: bool = True, **packing: Any) -> list[dict]:
+    """PnP packer -> FFA masks: every emitted bin becomes one
+    max_length-token sequence whose documents are placed back to back, each
+    attending only within itself (FULL, or CAUSAL for odd positions when
+    ``causal_odd``, the config-4 convention); the unfilled tail is padding
+    with no slice, so its rows give O = 0, LSE = -inf."""
+    out = []
+    for docs in pack_samples(lengths, max_length, bins, pool_capacity, **packing):
+        sl, off = [], 0
+        for i, n in enumerate(docs):
+            sl.append({"q": [off, off + n], "k": [off, off + n],
+                       "type": "causal" if causal_odd and i % 2 else "full"})
+            off += n
+        out.append({"seqlen_q": max_length, "seqlen_k": max_length, "slices": sl})
+    return out

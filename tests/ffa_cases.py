@@ -37,6 +37,10 @@ CASES = {
     "causal_lq_gt_lk": (400, 300, 1, 1, 64, [[0, 400]], [[0, 300]], [CAUSAL]),
     "sliding_window": (640, 640, 2, 1, 128, [[0, 96], [96, 640]], [[0, 96], [1, 640]], [CAUSAL, BI]),
     # keys [0,128), [300,400), [450,512) in no slice: dK/dV must come back 0
+    # a PnP-packed bin (planner.packed_bin_masks(lognormal_lengths(200, 150, 0.8,
+    # 1024, 5), 1024, 2, pool_capacity=32)[3]): 5 documents, 7-row padding tail
+    "packed_bin_padding_tail": (1024, 1024, 4, 2, 128,
+                                *varlen([299, 237, 222, 200, 59], [FULL, CAUSAL, FULL, CAUSAL, FULL])),
     "uncovered_keys": (256, 512, 2, 1, 128, [[0, 256], [0, 100]], [[128, 300], [400, 450]],
                        [FULL, CAUSAL]),
     # zero-length q or k ranges next to real slices (legal: qs <= qe, ks <= ke)

@@ -159,3 +159,20 @@ def test_pack_invariants(P):
     assert rep["stats"]["min_utilization"] >= 0.5  # the default defer_threshold
     docs = P.pack_samples(lengths[:200], 32768, 2)
     assert all(sum(d) <= 32768 for d in docs)
+
+
+def test_packed_bin_masks(P):
+    """Packer output as FFA masks: documents back to back, padding tail
+    without slices, MULTIPLICITY area = sum of per-document areas."""
+    lengths = P.lognormal_lengths(400, 2048.0, 1.0, 16384, 7)
+    masks = P.packed_bin_masks(lengths, 16384, 4)
+    assert masks
+    for spec in masks:
+        m = P.Mask(spec)
+        want, end = 0, 0
+        for i, (q, k, ty) in enumerate(m.slices):
+            n = q[1] - q[0]
+            assert q == k and q[0] == end and ty == (1 if i % 2 else 0)
+            want += n * n if ty == 0 else n * (n + 1) // 2
+            end = q[1]
+        assert end <= 16384 and m.area() == want == m.area(union=True)
