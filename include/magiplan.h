@@ -123,6 +123,13 @@ MAGIPLAN_API void magiplan_ffa_plan_free(magiplan_ffa_plan* plan);
 MAGIPLAN_API magiplan_status magiplan_ffa_plan_describe(const magiplan_ffa_plan* plan,
                                                         char** out_json);
 
+/* Uploads the plan's work lists to the current CUDA device (synchronous
+ * cudaMalloc + cudaMemcpy). Optional: the first launch on a plan does it
+ * otherwise, which then blocks that launch's host thread. A plan belongs to
+ * the device it was first uploaded to; launching it on another device is a
+ * MAGIPLAN_ERR_USAGE. */
+MAGIPLAN_API magiplan_status magiplan_ffa_plan_prepare(magiplan_ffa_plan* plan);
+
 /* Forward. q: [seqlen_q, num_heads_q, head_dim] bf16; k, v: [seqlen_k,
  * num_heads_k, head_dim] bf16 (GQA: num_heads_q % num_heads_k == 0);
  * out: [seqlen_q, num_heads_q, head_dim] in out_dtype; lse: [num_heads_q,

@@ -43,6 +43,7 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_ffa_plan_from_mask": (C.c_int, [_vp, _i32, C.POINTER(_vp)]),
     "magiplan_ffa_plan_free": (None, [_vp]),
     "magiplan_ffa_plan_describe": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "magiplan_ffa_plan_prepare": (C.c_int, [_vp]),
     "magiplan_ffa_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_ffa_bwd_preprocess": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp]),
     "magiplan_ffa_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),

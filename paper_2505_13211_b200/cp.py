@@ -75,6 +75,16 @@ def _stage_layouts(xplan: dict, rank: int, key: str) -> list[StageLayout]:
     return out
 
 
+def _new_group(ranks: list[int]):
+    """A second NCCL communicator over the same ranks, on high-priority
+    streams. Collective: every rank calls it in the same order."""
+    opts = None
+    if dist.get_backend() == "nccl":
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+    return dist.new_group(ranks=ranks, pg_options=opts)
+
+
 def _ranges_tensor(ranges: list[tuple[int, int]], device) -> tuple[torch.Tensor, torch.Tensor]:
     r = torch.tensor(ranges if ranges else [[0, 0]], dtype=torch.int64).reshape(-1, 2)
     lens = (r[:, 1] - r[:, 0]).tolist() if ranges else [0]
@@ -122,9 +132,50 @@ class CPAttention:
                 rr = [st.send_ranges[i] for i in st.send_by_dst[dst]]
                 per_dst.append(_ranges_tensor(rr, self.device) + (sum(b - a for a, b in rr),))
             st.dev["per_dst"] = per_dst
-        self.comm_stream = torch.cuda.Stream(self.device)
-        self.reduce_stream = torch.cuda.Stream(self.device)
+        # Work lists go to the device now (one synchronous upload per plan),
+        # not inside the first step that launches them.
+        for pl in [self.host_plan] + [st.plan for st in self.fwd_stages + self.bwd_stages]:
+            if pl is not None:
+                with torch.cuda.device(self.device):
+                    pl.prepare()
+        # High-priority streams: the block scheduler hands freed SMs to the
+        # gather / scatter-add / NCCL kernels ahead of queued FFA CTAs, the
+        # B200 counterpart of the paper's "communication kernel picked first"
+        # (footnote 7).
+        lo, hi = torch.cuda.Stream.priority_range()
+        self.comm_stream = torch.cuda.Stream(self.device, priority=hi)
+        self.reduce_stream = torch.cuda.Stream(self.device, priority=hi)
+        self._probe_stream = torch.cuda.Stream(self.device)
+        # GroupCast and GroupReduce on two communicators, so the all-to-alls
+        # of cast(j+1) and reduce(j-1) run concurrently instead of queueing on
+        # one NCCL stream (footnote 8).
+        self.cast_group, self.reduce_group = self.group, self.group
+        if self.world > 1:
+            ranks = dist.get_process_group_ranks(group) if group is not None else list(range(self.world))
+            self.cast_group = _new_group(ranks)
+            self.reduce_group = _new_group(ranks)
         self.L = _lib.lib()
+        self.timeline: list | None = None  # set to [] to record per-stage CUDA events
+
+    # ------------------------------------------------------------ tracing
+    def _ev(self, stream):
+        if self.timeline is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    def _span(self, pass_, task, j, e0, e1):
+        if self.timeline is not None:
+            self.timeline.append((pass_, task, j, e0, e1))
+
+    def timeline_ms(self, origin: "torch.cuda.Event") -> list[dict]:
+        """Recorded spans in ms relative to `origin` (after a synchronize)."""
+        out = []
+        for pass_, task, j, e0, e1 in self.timeline or []:
+            out.append({"pass": pass_, "task": task, "stage": j,
+                        "start_ms": origin.elapsed_time(e0), "end_ms": origin.elapsed_time(e1)})
+        return out
 
     # ------------------------------------------------------------ data layout
     def local_token_index(self) -> torch.Tensor:
@@ -146,8 +197,14 @@ class CPAttention:
         return out
 
     def _cast(self, st: StageLayout, k: torch.Tensor, v: torch.Tensor):
-        """GroupCast of stage `st` on the comm stream; returns (k_buf, v_buf, works)."""
+        """GroupCast of stage `st`: range gather on the comm stream, then the
+        all-to-all on the cast communicator. Returns (k_buf, v_buf, works,
+        send buffers, start event). The send buffers must outlive the works:
+        callers keep them until the compute stream has waited on every work
+        of the pass (so reuse by a later gather on the comm stream, which
+        first waits on the compute stream, is ordered after the NCCL read)."""
         with torch.cuda.stream(self.comm_stream):
+            e0 = self._ev(self.comm_stream)
             ks = self._gather(k, st, self.comm_stream)
             vs = self._gather(v, st, self.comm_stream)
             kb = torch.empty((st.buf_tokens, self.hk, self.d), dtype=k.dtype, device=k.device)
@@ -155,26 +212,47 @@ class CPAttention:
             works = []
             if self.world > 1:
                 works.append(dist.all_to_all_single(kb, ks, st.recv_splits, st.send_splits,
-                                                    group=self.group, async_op=True))
+                                                    group=self.cast_group, async_op=True))
                 works.append(dist.all_to_all_single(vb, vs, st.recv_splits, st.send_splits,
-                                                    group=self.group, async_op=True))
-        return kb, vb, works, (ks, vs)
+                                                    group=self.cast_group, async_op=True))
+        return kb, vb, works, (ks, vs), e0
+
+    def _cast_done(self, pass_, j, works, e0):
+        """Make the compute stream wait for a GroupCast; trace its end."""
+        cur = torch.cuda.current_stream(self.device)
+        if self.timeline is not None:
+            with torch.cuda.stream(self._probe_stream):
+                self._probe_stream.wait_stream(self.comm_stream)
+                for w in works:
+                    w.wait()
+                self._span(pass_, "cast", j, e0, self._ev(self._probe_stream))
+        for w in works:
+            w.wait()
+        cur.wait_stream(self.comm_stream)
 
     def _reduce(self, st: StageLayout, dk_buf, dv_buf, dk, dv):
-        """GroupReduce of a stage's f32 partial dK/dV into the hosts' dK/dV."""
+        """GroupReduce of a stage's f32 partial dK/dV into the hosts' dK/dV:
+        the transposed all-to-all on the reduce communicator (asynchronous;
+        the reduce stream waits on it), then one scatter-add per source rank
+        in rank order (deterministic sums). Returns the receive buffers,
+        which the caller keeps alive until the pass ends."""
         with torch.cuda.stream(self.reduce_stream):
             rows = sum(st.send_splits)
             rk = torch.empty((rows, self.hk, self.d), dtype=torch.float32, device=dk.device)
             rv = torch.empty_like(rk)
             if self.world > 1:
-                dist.all_to_all_single(rk, dk_buf, st.send_splits, st.recv_splits, group=self.group)
-                dist.all_to_all_single(rv, dv_buf, st.send_splits, st.recv_splits, group=self.group)
+                works = [dist.all_to_all_single(rk, dk_buf, st.send_splits, st.recv_splits,
+                                                group=self.reduce_group, async_op=True),
+                         dist.all_to_all_single(rv, dv_buf, st.send_splits, st.recv_splits,
+                                                group=self.reduce_group, async_op=True)]
+                for w in works:
+                    w.wait()
             base = 0
             row_elems = self.hk * self.d
+            sp = self.reduce_stream.cuda_stream
             for dst in range(self.world):  # fixed source-rank order => deterministic sums
                 ranges, offs, n = st.dev["per_dst"][dst]
                 if n:
-                    sp = self.reduce_stream.cuda_stream
                     for part, acc in ((rk, dk), (rv, dv)):
                         _lib.check(self.L.magiplan_range_scatter_add_f32(
                             part[base:].data_ptr(), acc.data_ptr(), ranges.data_ptr(), offs.data_ptr(),
@@ -193,85 +271,104 @@ class CPAttention:
         lse = torch.empty((self.hq, L), dtype=torch.float32, device=q.device)
         cur = torch.cuda.current_stream(q.device)
         self.comm_stream.wait_stream(cur)
+        keep = []  # receive and send buffers of every stage, until the pass ends
+        # step 0: cast(1) is issued first, then the host-local FFA
         pending = self._cast(self.fwd_stages[0], k, v) if self.fwd_stages else None
+        e0 = self._ev(cur)
         if self.host_plan is not None:
             ffa_forward(self.host_plan, q, k, v, self.scale, out=out, lse=lse)
         else:
             out.zero_()
             lse.fill_(-math.inf)
+        self._span("fwd", "ffa", 0, e0, self._ev(cur))
         for j, st in enumerate(self.fwd_stages):
-            kb, vb, works, keep = pending
+            kb, vb, works, sent, ec = pending
+            keep.append((kb, vb, sent))
+            # step j+1: cast(j+2) || ffa(j+1)
             if j + 1 < len(self.fwd_stages):
                 pending = self._cast(self.fwd_stages[j + 1], k, v)
-            for w in works:
-                w.wait()
-            cur.wait_stream(self.comm_stream)
+            self._cast_done("fwd", j + 1, works, ec)
+            e0 = self._ev(cur)
             if st.plan is not None:
                 ffa_forward(st.plan, q, kb, vb, self.scale, out=out, lse=lse, accumulate=True)
-            kb.record_stream(cur)
-            vb.record_stream(cur)
+            self._span("fwd", "ffa", j + 1, e0, self._ev(cur))
         out_bf = torch.empty((L, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
         _lib.check(self.L.magiplan_cast_f32_bf16(out.data_ptr(), out_bf.data_ptr(), out.numel(),
                                                  cur.cuda_stream))
+        for kb, vb, (ks, vs) in keep:  # stream-ordered frees after the compute stream's last use
+            for t in (kb, vb):
+                t.record_stream(cur)
         return out_bf, lse, out
 
     # ------------------------------------------------------------ backward
     def backward(self, q, k, v, out_f32, lse, dout):
         """Returns (dq, dk, dv) bf16 local shards."""
-        from .ffa import ffa_backward
-
         L = self.local_tokens
         dev = q.device
         cur = torch.cuda.current_stream(dev)
         sp = cur.cuda_stream
+        Ld = self.L
         delta = torch.empty((self.hq, L), dtype=torch.float32, device=dev)
-        _lib.check(self.L.magiplan_ffa_bwd_preprocess(out_f32.data_ptr(), dout.data_ptr(),
-                                                      delta.data_ptr(), L, self.hq, self.d, _lib.F32, sp))
         dq = torch.empty((L, self.hq, self.d), dtype=torch.float32, device=dev)
         dk = torch.empty((L, self.hk, self.d), dtype=torch.float32, device=dev)
         dv = torch.empty_like(dk)
         self.comm_stream.wait_stream(cur)
+        keep = []
+        # step 0: cast(1) first, then preprocess + host-local dQ / dK / dV
         pending = self._cast(self.bwd_stages[0], k, v) if self.bwd_stages else None
+        e0 = self._ev(cur)
+        _lib.check(Ld.magiplan_ffa_bwd_preprocess(out_f32.data_ptr(), dout.data_ptr(),
+                                                  delta.data_ptr(), L, self.hq, self.d, _lib.F32, sp))
         if self.host_plan is not None:
-            ffa_backward(self.host_plan, q, k, v, out_f32, lse, dout, self.scale, delta=delta,
-                         dq=dq, dk=dk, dv=dv)
+            _lib.check(Ld.magiplan_ffa_bwd(self.host_plan.handle, q.data_ptr(), k.data_ptr(),
+                                           v.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                           dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(),
+                                           self.hq, self.hk, self.scale, _lib.F32, 0, sp))
         else:
             dq.zero_()
             dk.zero_()
             dv.zero_()
-        self.reduce_stream.wait_stream(cur)  # dk/dv initialised before any scatter-add
-        keep = []
+        self._span("bwd", "ffa", 0, e0, self._ev(cur))
         for j, st in enumerate(self.bwd_stages):
-            kb, vb, works, sent = pending
+            kb, vb, works, sent, ec = pending
+            # step j+1: cast(j+2) || ffa(j+1) || reduce(j), the reduce having
+            # been issued on its own stream right after ffa(j)
             if j + 1 < len(self.bwd_stages):
                 pending = self._cast(self.bwd_stages[j + 1], k, v)
-            for w in works:
-                w.wait()
-            cur.wait_stream(self.comm_stream)
-            dkb = torch.zeros((st.buf_tokens, self.hk, self.d), dtype=torch.float32, device=dev)
-            dvb = torch.zeros_like(dkb)
+            self._cast_done("bwd", j + 1, works, ec)
+            # the dK/dV pass writes every row of its partial buffers (keys no
+            # slice reaches get zeros), so they need no initialisation
+            dkb = torch.empty((st.buf_tokens, self.hk, self.d), dtype=torch.float32, device=dev)
+            dvb = torch.empty_like(dkb)
+            e0 = self._ev(cur)
             if st.plan is not None:
-                Ld = self.L
-                _lib.check(Ld.magiplan_ffa_bwd_dq(st.plan.handle, q.data_ptr(), kb.data_ptr(),
-                                                  vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
-                                                  dout.data_ptr(), dq.data_ptr(), self.hq, self.hk,
-                                                  self.scale, _lib.F32, 1, sp))
+                # dK/dV of the received keys (fresh partials), then dQ added
+                # into the running dQ of the earlier stages
                 _lib.check(Ld.magiplan_ffa_bwd_dkdv(st.plan.handle, q.data_ptr(), kb.data_ptr(),
                                                     vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
                                                     dout.data_ptr(), dkb.data_ptr(), dvb.data_ptr(),
                                                     self.hq, self.hk, self.scale, _lib.F32, 0, sp))
-            kb.record_stream(cur)
-            vb.record_stream(cur)
-            self.reduce_stream.wait_stream(cur)
-            keep.append(self._reduce(st, dkb, dvb, dk, dv))
-            dkb.record_stream(self.reduce_stream)
-            dvb.record_stream(self.reduce_stream)
+                _lib.check(Ld.magiplan_ffa_bwd_dq(st.plan.handle, q.data_ptr(), kb.data_ptr(),
+                                                  vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                                  dout.data_ptr(), dq.data_ptr(), self.hq, self.hk,
+                                                  self.scale, _lib.F32, 1, sp))
+            else:
+                dkb.zero_()
+                dvb.zero_()
+            self._span("bwd", "ffa", j + 1, e0, self._ev(cur))
+            self.reduce_stream.wait_stream(cur)  # partial dK/dV of this stage (and dk/dv) ready
+            er = self._ev(self.reduce_stream)
+            recv = self._reduce(st, dkb, dvb, dk, dv)
+            self._span("bwd", "reduce", j + 1, er, self._ev(self.reduce_stream))
+            keep.append((kb, vb, sent, dkb, dvb, recv))
         cur.wait_stream(self.reduce_stream)
         outs = []
         for t in (dq, dk, dv):
             b = torch.empty(t.shape, dtype=torch.bfloat16, device=dev)
             _lib.check(self.L.magiplan_cast_f32_bf16(t.data_ptr(), b.data_ptr(), t.numel(), sp))
             outs.append(b)
+        # buffers allocated on the comm / reduce streams are freed here, after
+        # the compute stream has waited on every NCCL work that touched them
         del keep
         return tuple(outs)
 

@@ -136,6 +136,11 @@ magiplan_status magiplan_ffa_plan_describe(const magiplan_ffa_plan* plan, char**
   return guarded([&] { *out_json = dup_string(plan->plan.describe_json()); });
 }
 
+magiplan_status magiplan_ffa_plan_prepare(magiplan_ffa_plan* plan) {
+  MAGI_REQUIRE(plan);
+  return guarded([&] { magiplan::ensure_uploaded(plan->plan); });
+}
+
 magiplan_status magiplan_ffa_fwd(const magiplan_ffa_plan* plan, const void* q, const void* k,
                                  const void* v, void* out, float* lse, int64_t num_heads_q,
                                  int64_t num_heads_k, float softmax_scale, int32_t out_dtype,

@@ -65,6 +65,11 @@ class FFAPlan:
         _lib.check(_lib.lib().magiplan_ffa_plan_describe(self._handle, C.byref(out)))
         return json.loads(_lib.take_string(out))
 
+    def prepare(self) -> None:
+        """Upload the work lists to the current CUDA device now
+        (magiplan_ffa_plan_prepare) instead of inside the first launch."""
+        _lib.check(_lib.lib().magiplan_ffa_plan_prepare(self._handle))
+
     def area(self) -> int:
         return int(self.describe()["area_multiplicity"])
 
@@ -87,6 +92,23 @@ def _check_qkv(plan: FFAPlan, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor)
         raise ValueError("head_dim does not match the plan")
 
 
+def _check_buf(name: str, t: torch.Tensor, shape: tuple, device: torch.device,
+               dtypes: tuple = (torch.float32, torch.bfloat16)) -> None:
+    """Caller-supplied output / auxiliary buffers are written through raw
+    pointers: a wrong shape, dtype, device or layout is a ValueError here,
+    never an out-of-bounds device write."""
+    if not torch.is_tensor(t):
+        raise ValueError(f"{name} must be a tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(t.shape)}")
+    if t.dtype not in dtypes:
+        raise ValueError(f"{name} must be one of {dtypes}, got {t.dtype}")
+    if t.device != device:
+        raise ValueError(f"{name} must be on {device}, got {t.device}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
 def ffa_forward(plan: FFAPlan, q, k, v, softmax_scale: float | None = None, *,
                 out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
                 out_dtype: torch.dtype = torch.bfloat16, accumulate: bool = False):
@@ -104,10 +126,13 @@ def ffa_forward(plan: FFAPlan, q, k, v, softmax_scale: float | None = None, *,
         out = torch.empty((sq, hq, d), dtype=out_dtype, device=q.device)
     if lse is None:
         lse = torch.empty((hq, sq), dtype=torch.float32, device=q.device)
+    _check_buf("out", out, (sq, hq, d), q.device)
+    _check_buf("lse", lse, (hq, sq), q.device, (torch.float32,))
     dt = _lib.F32 if out.dtype == torch.float32 else _lib.BF16
-    _lib.check(_lib.lib().magiplan_ffa_fwd(
-        plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr(),
-        hq, hk, scale, dt, int(accumulate), _stream_ptr(q.device)))
+    with torch.cuda.device(q.device):  # plan upload and launch on q's device
+        _lib.check(_lib.lib().magiplan_ffa_fwd(
+            plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), lse.data_ptr(),
+            hq, hk, scale, dt, int(accumulate), _stream_ptr(q.device)))
     return out, lse
 
 
@@ -122,31 +147,40 @@ def ffa_backward(plan: FFAPlan, q, k, v, out, lse, dout, softmax_scale: float | 
     dev = q.device
     stream = _stream_ptr(dev)
     L = _lib.lib()
-    if dout.dtype != torch.bfloat16 or not dout.is_contiguous():
-        raise ValueError("dout must be a contiguous bf16 tensor")
-    if delta is None:
-        delta = torch.empty((hq, sq), dtype=torch.float32, device=dev)
-        _lib.check(L.magiplan_ffa_bwd_preprocess(
-            out.data_ptr(), dout.data_ptr(), delta.data_ptr(), sq, hq, d,
-            _lib.F32 if out.dtype == torch.float32 else _lib.BF16, stream))
-    if dq is None:
-        dq = torch.empty((sq, hq, d), dtype=grad_dtype, device=dev)
-    if dk is None:
-        dk = torch.empty((sk, hk, d), dtype=grad_dtype, device=dev)
-    if dv is None:
-        dv = torch.empty((sk, hk, d), dtype=grad_dtype, device=dev)
-    gdt = _lib.F32 if dq.dtype == torch.float32 else _lib.BF16
-    _lib.check(L.magiplan_ffa_bwd(
-        plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(), delta.data_ptr(),
-        dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), hq, hk, scale, gdt,
-        int(accumulate), stream))
+    _check_buf("out", out, (sq, hq, d), dev)
+    _check_buf("lse", lse, (hq, sq), dev, (torch.float32,))
+    _check_buf("dout", dout, (sq, hq, d), dev, (torch.bfloat16,))
+    with torch.cuda.device(dev):  # plan upload and launches on q's device
+        if delta is None:
+            delta = torch.empty((hq, sq), dtype=torch.float32, device=dev)
+            _lib.check(L.magiplan_ffa_bwd_preprocess(
+                out.data_ptr(), dout.data_ptr(), delta.data_ptr(), sq, hq, d,
+                _lib.F32 if out.dtype == torch.float32 else _lib.BF16, stream))
+        _check_buf("delta", delta, (hq, sq), dev, (torch.float32,))
+        if dq is None:
+            dq = torch.empty((sq, hq, d), dtype=grad_dtype, device=dev)
+        if dk is None:
+            dk = torch.empty((sk, hk, d), dtype=grad_dtype, device=dev)
+        if dv is None:
+            dv = torch.empty((sk, hk, d), dtype=grad_dtype, device=dev)
+        _check_buf("dq", dq, (sq, hq, d), dev)
+        _check_buf("dk", dk, (sk, hk, d), dev, (dq.dtype,))
+        _check_buf("dv", dv, (sk, hk, d), dev, (dq.dtype,))
+        gdt = _lib.F32 if dq.dtype == torch.float32 else _lib.BF16
+        _lib.check(L.magiplan_ffa_bwd(
+            plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+            dout.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), hq, hk, scale, gdt,
+            int(accumulate), stream))
     return dq, dk, dv
 
 
 _PLAN_CACHE: dict = {}
 
 
-def get_plan(q_ranges, k_ranges, types, seqlen_q, seqlen_k, head_dim) -> FFAPlan:
+def get_plan(q_ranges, k_ranges, types, seqlen_q, seqlen_k, head_dim,
+             device: torch.device | None = None) -> FFAPlan:
+    """Cached plan per (slice list, sizes, device): a plan's work lists live
+    on the device of its first launch (magiplan_ffa_plan_prepare)."""
     qr = np.asarray(q_ranges.cpu() if torch.is_tensor(q_ranges) else q_ranges, dtype=np.int64)
     kr = np.asarray(k_ranges.cpu() if torch.is_tensor(k_ranges) else k_ranges, dtype=np.int64)
     if types is None:
@@ -154,7 +188,8 @@ def get_plan(q_ranges, k_ranges, types, seqlen_q, seqlen_k, head_dim) -> FFAPlan
     else:
         ty = np.asarray(types.cpu() if torch.is_tensor(types) else
                         [SLICE_TYPES[t] if isinstance(t, str) else int(t) for t in types], dtype=np.int32)
-    key = (qr.tobytes(), kr.tobytes(), ty.tobytes(), int(seqlen_q), int(seqlen_k), int(head_dim))
+    key = (qr.tobytes(), kr.tobytes(), ty.tobytes(), int(seqlen_q), int(seqlen_k), int(head_dim),
+           str(device))
     plan = _PLAN_CACHE.get(key)
     if plan is None:
         plan = FFAPlan(qr, kr, ty, seqlen_q, seqlen_k, head_dim)
@@ -189,5 +224,5 @@ def flex_flash_attn_func(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, q_ra
     half-open token ranges; attn_type_map: [n] of 0 full, 1 causal,
     2 inv_causal, 3 bi_causal (default all full). Differentiable w.r.t. q, k, v.
     """
-    plan = get_plan(q_ranges, k_ranges, attn_type_map, q.shape[0], k.shape[0], q.shape[2])
+    plan = get_plan(q_ranges, k_ranges, attn_type_map, q.shape[0], k.shape[0], q.shape[2], q.device)
     return _FlexFlashAttn.apply(q, k, v, plan, softmax_scale)

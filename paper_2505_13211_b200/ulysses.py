@@ -88,20 +88,35 @@ class UlyssesAttention:
         lse_h = torch.full((hl, S), -math.inf, dtype=torch.float32, device=q.device)
         if self.plan is not None:
             ffa_forward(self.plan, qh, kh, vh, self.scale, out=out_h, lse=lse_h)
-        self._saved = (qh, kh, vh, out_h, lse_h)
         out32 = _heads_to_tokens(out_h, w, g)
         # lse [hl, S] -> token-major [S, hl] for the exchange, then back to [hq, L]
         lse = _heads_to_tokens(lse_h.t().contiguous(), w, g).t().contiguous()
         out = torch.empty((self.local_tokens, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
         stream = torch.cuda.current_stream(q.device).cuda_stream
         _lib.check(self.L.magiplan_cast_f32_bf16(out32.data_ptr(), out.data_ptr(), out32.numel(), stream))
+        # the head-sharded tensors are reused by the backward of THIS forward
+        # only: keyed by the identity and version of every tensor involved
+        self._saved = ((q, k, v, out32, lse), [t._version for t in (q, k, v, out32, lse)],
+                       (qh, kh, vh, out_h, lse_h))
         return out, lse, out32
+
+    def _matches(self, ts) -> bool:
+        saved = getattr(self, "_saved", None)
+        return (saved is not None and all(a is b for a, b in zip(saved[0], ts))
+                and saved[1] == [t._version for t in ts])
 
     def backward(self, q, k, v, out_f32, lse, dout):
         """dQ, dK, dV (bf16, this rank's token shard). Reuses the head-sharded
-        tensors of the preceding forward."""
+        tensors of the forward that produced (out_f32, lse) when these are
+        its outputs for the same q/k/v; otherwise (another forward ran in
+        between, or different inputs) they are exchanged again from the
+        arguments."""
         w, g = self.world, self.group
-        qh, kh, vh, out_h, lse_h = self._saved
+        if self._matches((q, k, v, out_f32, lse)):
+            qh, kh, vh, out_h, lse_h = self._saved[2]
+        else:
+            qh, kh, vh, out_h = (_tokens_to_heads(t, w, g) for t in (q, k, v, out_f32))
+            lse_h = _tokens_to_heads(lse.t().contiguous(), w, g).t().contiguous()
         doh = _tokens_to_heads(dout, w, g)
         if self.plan is None:
             dqh = torch.zeros(qh.shape, dtype=torch.float32, device=q.device)

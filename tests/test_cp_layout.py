@@ -35,7 +35,20 @@ MASKS = [
 ]
 
 
-def scenario(mask, cp, chunk, min_chunk=16, max_chunks=5):
+# A cost model under which splitting is free and the cast is expensive: the
+# overlap solver then takes as many stages as there are packages, so
+# `max_num_chunks` forces the stage count (Alg. 2, overlap.cpp:343-399).
+COST_STAGED = {"ffa_fwd": {"latency": 0, "per_unit": 8.19e-05}, "ffa_bwd": {"latency": 0, "per_unit": 2.05e-04},
+               "cast": {"latency": 0, "per_unit": 0.082}, "reduce": {"latency": 0, "per_unit": 0.082}}
+
+
+def scenario(mask, cp, chunk, min_chunk=16, max_chunks=5, stages=None):
+    """stages=None: the default cost model (one stage on these sizes);
+    stages=s: COST_STAGED with s packages, i.e. up to s fwd / bwd stages."""
+    if stages is not None:
+        return {"workload": {"mask": mask, "num_heads_q": 4, "num_heads_k": 2}, "cp_size": cp,
+                "dispatch_chunk_size": chunk, "cost_model": COST_STAGED,
+                "overlap": {"min_chunk_size": 4, "max_num_chunks": stages}}
     return {"workload": {"mask": mask, "num_heads_q": 4, "num_heads_k": 2}, "cp_size": cp,
             "dispatch_chunk_size": chunk, "cost_model": COST,
             "overlap": {"min_chunk_size": min_chunk, "max_num_chunks": max_chunks}}
@@ -50,12 +63,16 @@ def dense(sq, sk, slices):
     return oracle.dense_allowed(sq, sk, qr, kr, ty) if slices else np.zeros((sq, sk), np.int32)
 
 
+@pytest.mark.parametrize("stages", [None, 3, 4])
 @pytest.mark.parametrize("idx", range(len(MASKS)))
-def test_exec_plan_covers_each_rank_exactly(built_lib, idx):
+def test_exec_plan_covers_each_rank_exactly(built_lib, idx, stages):
     from paper_2505_13211_b200.planner import Mask, Scenario
 
     mask, cp, chunk = MASKS[idx]
-    xp = Scenario(scenario(mask, cp, chunk)).exec_plan()
+    xp = Scenario(scenario(mask, cp, chunk, stages=stages)).exec_plan()
+    if stages is not None:  # the multi-stage schedule is really planned
+        assert xp["num_stages_bwd"] >= 3, xp["num_stages_bwd"]
+        assert max(len(st["recv"]) for r in xp["ranks"] for st in r["bwd_stages"]) >= 2
     m = Mask(mask)
     S = m.seqlen_q
     glob = dense(S, S, [[*q, *k, t] for q, k, t in m.slices])
@@ -85,12 +102,12 @@ def test_exec_plan_covers_each_rank_exactly(built_lib, idx):
             np.testing.assert_array_equal(got[q_glob], glob[q_glob])
             if key == "fwd_stages":
                 recv = sum(st["buf_tokens"] for st in r[key])
-                plan = Scenario(scenario(mask, cp, chunk)).plan()
+                plan = Scenario(scenario(mask, cp, chunk, stages=stages)).plan()
                 src_recv = plan["transfer_cast"]["sources"][r["rank"]]["recv_tokens"]
                 assert recv == src_recv  # zero redundancy: exactly the planned GroupCast volume
 
 
-def _exchange_worker(rank, world, port, mask, chunk, q):
+def _exchange_worker(rank, world, port, mask, chunk, q, stages=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -98,11 +115,11 @@ def _exchange_worker(rank, world, port, mask, chunk, q):
         from paper_2505_13211_b200.cp import _stage_layouts
         from paper_2505_13211_b200.planner import Scenario
 
-        xp = Scenario(scenario(mask, world, chunk)).exec_plan()
+        xp = Scenario(scenario(mask, world, chunk, stages=stages)).exec_plan()
+        ok = stages is None or (xp["num_stages_fwd"] >= 2 and xp["num_stages_bwd"] >= 2)
         me = xp["ranks"][rank]
         cs = xp["chunk_size"]
         ids = torch.tensor([c * cs + t for c in me["chunks"] for t in range(cs)], dtype=torch.int64)
-        ok = True
         for key in ("fwd_stages", "bwd_stages"):
             for j, st in enumerate(_stage_layouts(xp, rank, key)):
                 send = torch.cat([ids[a:b] for a, b in st.send_ranges]) if st.send_ranges else \
@@ -124,14 +141,19 @@ def _exchange_worker(rank, world, port, mask, chunk, q):
         dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("stages", [None, 4])
 @pytest.mark.parametrize("world", [2, 4, 8])
-def test_groupcast_groupreduce_exchange_gloo(built_lib, world):
+def test_groupcast_groupreduce_exchange_gloo(built_lib, world, stages):
+    """Every stage's all-to-all delivers exactly the planned receive buffer
+    (and the transposed GroupReduce returns one partial per sent token),
+    with one stage and with the multi-stage split (stages=4: 2-4 fwd, 4 bwd)."""
     mask = {"seqlen": 512, "pattern": "varlen_block_causal", "params": {"sample_lengths": [256, 256],
                                                                         "block_size": 32}}
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + world
-    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, mask, 16, q)) for r in range(world)]
+    port = 29600 + world + (20 if stages else 0)
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, mask, 16, q, stages))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in range(world))

@@ -2,8 +2,9 @@
 
 Tolerance (bf16 inputs; P, dS rounded to bf16 as MMA operands; fp32
 accumulation; compared with a float64 oracle on the same bf16 inputs and the
-oracle's own O/LSE): max abs error <= 3% of max |grad| per tensor, computed
-on f32 gradient outputs; bf16 outputs are checked to 4%.
+oracle's own O/LSE): max abs error <= 1% of max |grad| per tensor, computed
+on f32 gradient outputs; bf16 outputs are checked to 1.5% (measured errors
+are printed; round 1 measured <= 0.33%).
 """
 import math
 
@@ -15,7 +16,7 @@ from tests.ffa_cases import CASES, err_stats, make_inputs
 
 pytestmark = pytest.mark.gpu
 
-REL_F32, REL_BF16 = 3e-2, 4e-2
+REL_F32, REL_BF16 = 1e-2, 1.5e-2
 
 
 def _run(name, grad_dtype, seed=1):
@@ -48,6 +49,7 @@ def test_bwd_matches_oracle_f32(built_lib, cuda, name):
 @pytest.mark.parametrize("name", ["block_causal_gqa_d128", "varlen_mixed", "cfg1_block_causal_d64"])
 def test_bwd_matches_oracle_bf16(built_lib, cuda, name):
     res = _run(name, torch.bfloat16, seed=4)
+    print(name, "bf16", {k: f"abs {a:.2e} rel {r:.2e}" for k, (a, r) in res.items()})
     for nm, (_, rel) in res.items():
         assert rel <= REL_BF16, (nm, rel)
 

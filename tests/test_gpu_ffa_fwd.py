@@ -1,8 +1,9 @@
 """FFA forward parity: sm_100a kernel (through the C ABI) vs the CPU oracle.
 
 Tolerance (bf16 inputs, bf16 P operand, fp32 accumulation, bf16 output vs a
-float64 oracle on the same bf16-rounded inputs): O max abs error <= 2e-2 and
-<= 1% of max |O|; LSE max abs error <= 1e-3. Empty rows must be exactly
+float64 oracle on the same bf16-rounded inputs): O max abs error <= 1e-2 and
+<= 0.5% of max |O|; LSE max abs error <= 2e-4 (measured errors are printed;
+round 1 measured O <= 0.33%). Empty rows must be exactly
 O = 0, LSE = -inf.
 """
 import math
@@ -15,7 +16,7 @@ from tests.ffa_cases import CASES, err_stats, make_inputs
 
 pytestmark = pytest.mark.gpu
 
-O_ABS, O_REL, LSE_ABS = 2e-2, 1e-2, 1e-3
+O_ABS, O_REL, LSE_ABS = 1e-2, 5e-3, 2e-4
 
 
 @pytest.mark.parametrize("name", sorted(CASES))
@@ -106,7 +107,8 @@ def test_fwd_bwd_large_logits(built_lib, cuda, gain):
     assert o_abs <= O_ABS * 2 and o_rel <= O_REL * 2, (o_abs, o_rel)
     assert l_abs <= LSE_ABS * gain, l_abs
     rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ref_o, ref_lse, do, qr, kr, ty, scale)
-    for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
-        _, rel = err_stats(got.float().cpu().numpy(), ref)
-        assert rel <= 4e-2, rel
+    for nm, got, ref in (("dq", dq, rdq), ("dk", dk, rdk), ("dv", dv, rdv)):
+        a, rel = err_stats(got.float().cpu().numpy(), ref)
+        print(f"large logits x{gain}: {nm} abs {a:.2e} rel {rel:.2e}; O rel {o_rel:.2e}; LSE {l_abs:.2e}")
+        assert rel <= 2e-2, rel
     assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()

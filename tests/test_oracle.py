@@ -99,3 +99,31 @@ def test_oracle_numerics_vs_dense_float64(case):
     # the f32-accumulating variant used for the CPU baseline agrees to f32 precision
     of, lf = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale, acc_f32=True)
     np.testing.assert_allclose(of, o, atol=1e-5)
+
+
+@pytest.mark.parametrize("name", ["varlen_mixed", "inv_bi_d64", "overlap_multiplicity", "empty_rows",
+                                  "cross_lk_gt_lq", "causal_lq_gt_lk", "uncovered_keys", "sliding_window"])
+def test_dense_fp32_reference_matches_oracle(name):
+    """tests/dense_ref.py (the full-size GPU tests' fp32 reference, which
+    recomputes LSE / O / delta itself) agrees with the pinned oracle on the
+    slice-list edge cases: multiplicity, INV/BI types, empty rows, keys no
+    slice reaches, cross-length slices. Run on CPU here."""
+    from tests import dense_ref
+    from tests.ffa_cases import CASES, make_inputs
+
+    sq, sk, hq, hk, d, qr, kr, ty = CASES[name]
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=3, device="cpu")
+    scale = 1.0 / math.sqrt(d)
+    ro, rl = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale)
+    rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ro, rl, do, qr, kr, ty, scale)
+    slices = [(tuple(a), tuple(b), t) for a, b, t in zip(qr, kr, ty)]
+    out, lse = dense_ref.forward_all(q, k, v, slices, scale, rows_per_chunk=64)
+    rows, keys = list(range(0, sq, 7)), list(range(0, sk, 5))
+    o, l, dq = dense_ref.rows_ref(q, k, v, do, slices, scale, rows, lse, out)
+    dk, dv = dense_ref.keys_ref(q, k, v, do, slices, scale, keys, lse, out, rows_per_chunk=64)
+    fin = np.isfinite(rl)
+    assert np.array_equal(np.isfinite(lse.numpy()), fin)
+    assert np.abs(lse.numpy()[fin] - rl[fin]).max() < 1e-5
+    for got, ref in ((out.numpy(), ro), (dq.numpy(), rdq[rows]), (dk.numpy(), rdk[keys]),
+                     (dv.numpy(), rdv[keys])):
+        assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max())
