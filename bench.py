@@ -191,20 +191,81 @@ def cpu_baseline_sample(wl: dict, target_s: float = 12.0) -> dict:
             "seconds": dt}
 
 
+def host_info() -> dict:
+    model = ""
+    try:
+        for ln in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if ln.startswith("Model name"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
+def planner_timing(reps: int = 3) -> dict:
+    """The reference's own CPU path for CP planning (mask
+    sweep, greedy dispatch, KV demands, transfer tables, stage solve), timed
+    on this host through magiplan_scenario_parse + magiplan_scenario_plan:
+    the reference compiled from its sources (oracle/_ref, test
+    infrastructure) beside this library, plan JSON compared byte for byte.
+    Single-threaded, as the reference is."""
+    from tools import bench_planner as bp
+
+    if not bp.REF.exists():
+        return {"unavailable": "oracle/_ref/libmagiplan_ref.so not built"}
+    ours, ref = bp._bind(bp.OURS), bp._bind(bp.REF)
+    rows = []
+    for name, spec in bp.scenarios():
+        if "S=1048576 cp=8 block=8192" not in name and "S=524288" not in name and "S=131072" not in name:
+            continue
+        t_ours, ms_ours = bp._plan(ours, spec, reps)
+        t_ref, ms_ref = bp._plan(ref, spec, reps)
+        rows.append({"scenario": name, "reference_ms": round(statistics.median(ms_ref), 2),
+                     "ours_ms": round(statistics.median(ms_ours), 2), "identical_plan_json": t_ours == t_ref})
+    return {"what": "scenario_plan (shard + greedy + demands + tables + solve), 1 thread",
+            "cores": 1, **host_info(), "runs": rows}
+
+
+def single_config(workload: str) -> tuple[dict, tuple]:
+    """The N=1 line's `config` (shared by both arms) and the slice list."""
+    from paper_2505_13211_b200.planner import Mask
+
+    wl = WORKLOADS[workload]
+    S, hq, hk, d, block = wl["seqlen"], wl["hq"], wl["hk"], wl["d"], wl["block"]
+    if wl.get("varlen"):
+        qr, kr, ty = varlen_packed(S)
+        mask_desc = f"varlen packed FULL/CAUSAL, {len(qr)} samples (lognormal median 2048, sigma 1, seed 42)"
+    else:
+        qr, kr, ty = block_causal(S, block)
+        mask_desc = f"block_causal(block={block})"
+    names = {0: "full", 1: "causal", 2: "inv_causal", 3: "bi_causal"}
+    area = Mask({"seqlen_q": S, "seqlen_k": S, "slices": [{"q": a, "k": b, "type": names[t]}
+                                                           for a, b, t in zip(qr, kr, ty)]}).area()
+    fwd = 4 * area * hq * d
+    cfg = {"workload": workload, "seqlen": S, "num_heads_q": hq, "num_heads_k": hk, "head_dim": d,
+           "mask": mask_desc, "area_multiplicity": area, "flops_per_step": fwd + fwd * 5 // 2,
+           "parallelism": "single GPU",
+           "l2": f"inputs larger than L2 (q {S * hq * d * 2 / 1e6:.0f} MB, dO {S * hq * d * 2 / 1e6:.0f} MB "
+                 f"> 126 MB); no flush"}
+    return cfg, (qr, kr, ty)
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     wl = WORKLOADS[args.workload]
-    workload = args.workload
-    if args.gpus > 1:
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
+    if world > 1:
         # the N>1 arm's workload: the CP config-5 shape (cp_bench), per-rank
         # tokens x N, block-causal 8192; the CPU sample is bounded either way
         from paper_2505_13211_b200 import cp_bench
 
-        wl = dict(seqlen=cp_bench.PER_RANK * args.gpus, hq=cp_bench.HQ, hk=cp_bench.HK, d=cp_bench.D,
+        wl = dict(seqlen=cp_bench.PER_RANK * world, hq=cp_bench.HQ, hk=cp_bench.HK, d=cp_bench.D,
                   block=cp_bench.BLOCK)
-        workload = "cp_block_causal_magi1_24b"
+        config = cp_bench.config(world, args.cp_mode)
+    else:
+        config, _ = single_config(args.workload)
     for _ in range(args.warmup):
         cpu_baseline_sample(wl, target_s=2.0)
     vals, samples = [], []
@@ -215,12 +276,12 @@ def run_reference(args) -> None:
     value = statistics.median(vals)
     base = samples[-1]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": {"workload": workload, **wl, "mask": "block_causal"},
+        "config": config,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": "port",
-                         "sample": base["sample"]},
+                         "sample": base["sample"], **host_info(), "reference_planner": planner_timing()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -236,14 +297,11 @@ def run_single(args) -> None:
     S, hq, hk, d, block = wl["seqlen"], wl["hq"], wl["hk"], wl["d"], wl["block"]
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    if wl.get("varlen"):
-        qr, kr, ty = varlen_packed(S)
-        mask_desc = f"varlen packed FULL/CAUSAL, {len(qr)} samples (lognormal median 2048, sigma 1, seed 42)"
-    else:
-        qr, kr, ty = block_causal(S, block)
-        mask_desc = f"block_causal(block={block})"
+    config, (qr, kr, ty) = single_config(args.workload)
     plan = FFAPlan(qr, kr, ty, S, S, d)
+    plan.prepare()
     area = plan.area()
+    assert area == config["area_multiplicity"]
     if not wl.get("varlen"):
         assert area == block_causal_area(S, block)
     fwd_flops = 4 * area * hq * d
@@ -316,24 +374,26 @@ def run_single(args) -> None:
 
     # e2e through the public API with host buffers: H2D of the step's inputs,
     # forward + backward, D2H of the gradients.
+    o_h = torch.empty_like(out, device="cpu").pin_memory()
     dq_h = torch.empty_like(dq, device="cpu").pin_memory()
     dk_h = torch.empty_like(dk, device="cpu").pin_memory()
     dv_h = torch.empty_like(dv, device="cpu").pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in (q_h, k_h, v_h, do_h))
-    d2h = sum(t.numel() * t.element_size() for t in (dq_h, dk_h, dv_h))
+    d2h = sum(t.numel() * t.element_size() for t in (o_h, dq_h, dk_h, dv_h))
 
     # Two device buffer sets so step i+1's inputs travel (H2D stream) and step
-    # i-1's gradients return (D2H stream) while step i computes. Every step
-    # still copies its own inputs in and its gradients out through PCIe.
-    sets = [dict(q=q, k=k, v=v, do=do, dq=dq, dk=dk, dv=dv)]
+    # i-1's outputs return (D2H stream) while step i computes. Every step
+    # still copies its own inputs in and its O, dQ, dK, dV out through PCIe.
+    sets = [dict(q=q, k=k, v=v, do=do, out=out, dq=dq, dk=dk, dv=dv)]
     sets.append({n: torch.empty_like(t) for n, t in sets[0].items()})
     h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
-    def step_on(b, ev_do, ev_kv_done):
+    def step_on(b, ev_do, ev_fwd_done, ev_kv_done):
         _lib.check(L.magiplan_ffa_fwd(plan.handle, b["q"].data_ptr(), b["k"].data_ptr(), b["v"].data_ptr(),
-                                      out.data_ptr(), lse.data_ptr(), hq, hk, scale, BF, 0, sp))
+                                      b["out"].data_ptr(), lse.data_ptr(), hq, hk, scale, BF, 0, sp))
+        ev_fwd_done.record(stream)  # O can travel back while the backward computes
         stream.wait_event(ev_do)  # dO is only needed from the backward on
-        _lib.check(L.magiplan_ffa_bwd_preprocess(out.data_ptr(), b["do"].data_ptr(), delta.data_ptr(),
+        _lib.check(L.magiplan_ffa_bwd_preprocess(b["out"].data_ptr(), b["do"].data_ptr(), delta.data_ptr(),
                                                  S, hq, d, BF, sp))
         _lib.check(L.magiplan_ffa_bwd_dkdv(plan.handle, b["q"].data_ptr(), b["k"].data_ptr(),
                                            b["v"].data_ptr(), lse.data_ptr(), delta.data_ptr(),
@@ -346,7 +406,7 @@ def run_single(args) -> None:
 
     def e2e_run(n, start=None):
         mk = lambda: [torch.cuda.Event() for _ in range(n)]  # noqa: E731
-        ev_qkv, ev_do, ev_kv, ev_done, ev_out = mk(), mk(), mk(), mk(), mk()
+        ev_qkv, ev_do, ev_fwd, ev_kv, ev_done, ev_out = mk(), mk(), mk(), mk(), mk(), mk()
 
         def h2d(i):
             b = sets[i % 2]
@@ -368,10 +428,12 @@ def run_single(args) -> None:
             stream.wait_event(ev_qkv[i])
             if i >= 2:
                 stream.wait_event(ev_out[i - 2])  # gradients of this set already returned
-            step_on(sets[i % 2], ev_do[i], ev_kv[i])
+            step_on(sets[i % 2], ev_do[i], ev_fwd[i], ev_kv[i])
             ev_done[i].record(stream)
             with torch.cuda.stream(d2h_s):
                 b = sets[i % 2]
+                d2h_s.wait_event(ev_fwd[i])
+                o_h.copy_(b["out"], non_blocking=True)
                 d2h_s.wait_event(ev_kv[i])
                 dk_h.copy_(b["dk"], non_blocking=True)
                 dv_h.copy_(b["dv"], non_blocking=True)
@@ -413,24 +475,29 @@ def run_single(args) -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": args.workload, "seqlen": S, "num_heads_q": hq, "num_heads_k": hk,
-                   "head_dim": d, "mask": mask_desc, "area_multiplicity": area,
-                   "flops_per_step": step_flops, "parallelism": "single GPU",
-                   "l2": f"inputs larger than L2 (q {q.numel() * 2 / 1e6:.0f} MB, "
-                         f"dO {do.numel() * 2 / 1e6:.0f} MB > 126 MB); no flush"},
+        "config": config,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16"],
                      "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": traffic,
                      "peak_source": peaks["source"], "peak_sustained": peaks["bf16_sustained"],
                      "step_frac": value / peaks["bf16"]},
         "kernels": kernels,
         "e2e": {"value": step_flops / (e2e_ms * 1e-3) / 1e12, "unit": UNIT,
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+                "copies": "H2D q, k, v, dO; D2H O, dQ, dK, dV (bf16), every step"},
         "clocks": clk,
         "gpu_launches": launches_per_step * args.steps,
     }
+    del sets, q, k, v, do, out, dq, dk, dv
+    torch.cuda.empty_cache()
+    if not args.no_weak_anchor:
+        from paper_2505_13211_b200 import cp_bench
+
+        line["weak_anchor"] = cp_bench.anchor(steps=2, warmup=1)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_sample(wl)
         line["cpu_baseline"].pop("seconds", None)
+        line["cpu_baseline"].update(host_info())
+        line["cpu_baseline"]["reference_planner"] = planner_timing()
     print(json.dumps(line), flush=True)
 
 
@@ -442,6 +509,8 @@ def main() -> None:
     ap.add_argument("--impl", default="magi", choices=["magi", "reference"])
     ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-weak-anchor", action="store_true",
+                    help="N=1: skip the cp=1 run of the CP weak-scaling workload")
     ap.add_argument("--cp-mode", default="magi", choices=["magi", "ring", "ulysses"],
                     help="N>1 only: MagiAttention GroupCast CP (default), or the ring-attention / "
                          "Ulysses all-to-all baselines")

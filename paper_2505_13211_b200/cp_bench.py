@@ -43,6 +43,71 @@ def scenario(cp: int) -> dict:
                         "max_num_chunks": int(os.environ.get("MAGI_CP_MAX_CHUNKS", "8"))}}
 
 
+def config(world: int, mode: str = "magi") -> dict:
+    """The N>1 line's `config` (shared with the reference arm), computed on
+    the host from the planner alone."""
+    S = PER_RANK * world
+    if mode == "ring":
+        chunk, ns = S // (2 * world), (world, world)
+    elif mode == "ulysses":
+        chunk, ns = S // world, (1, 1)
+    else:
+        from .planner import Scenario
+
+        xp = Scenario(scenario(world)).exec_plan()
+        chunk, ns = xp["chunk_size"], (xp["num_stages_fwd"], xp["num_stages_bwd"])
+    area = block_causal_area(S, BLOCK)
+    fwd = 4 * area * HQ * D
+    return {"workload": "cp_block_causal_magi1_24b", "seqlen": S, "tokens_per_rank": PER_RANK,
+            "num_heads_q": HQ, "num_heads_k": HK, "head_dim": D, "mask": f"block_causal(block={BLOCK})",
+            "area_multiplicity": area, "flops_per_step": fwd + fwd * 5 // 2,
+            "dispatch": {"ring": "zigzag", "ulysses": "contiguous"}.get(mode, "greedy"), "cp_mode": mode,
+            "dispatch_chunk_size": chunk, "num_stages_fwd": ns[0], "num_stages_bwd": ns[1],
+            "parallelism": f"cp{world}", "l2": "inputs larger than L2 per rank; no flush"}
+
+
+def block_causal_area(S: int, block: int) -> int:
+    n = S // block
+    return n * (n + 1) // 2 * block * block
+
+
+def anchor(steps: int = 2, warmup: int = 1) -> dict:
+    """The weak-scaling anchor: the N>1 workload's per-rank shape at cp = 1
+    (131072 tokens, 48 q / 8 kv heads, block-causal 8192) through the same
+    CPAttention executor on one GPU (host-local FFA only). Weak efficiency at
+    N is tflops_per_gpu(N) / this value."""
+    from .cp import CPAttention
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    cpa = CPAttention(scenario(1), HQ, HK, D)
+    L = cpa.local_tokens
+    g = torch.Generator(device="cpu").manual_seed(1234)
+    q = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).to(dev)
+    k = torch.randn(L, HK, D, generator=g).to(torch.bfloat16).to(dev)
+    v = torch.randn(L, HK, D, generator=g).to(torch.bfloat16).to(dev)
+    do = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).to(dev)
+
+    def step():
+        out, lse, out32 = cpa.forward(q, k, v)
+        return cpa.backward(q, k, v, out32, lse, do)
+
+    for _ in range(warmup):
+        step()
+    stream = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    fwd, bwd = cpa.flops()
+    return {"what": "CP workload per-rank shape at cp=1 (weak-scaling anchor)", "config": config(1),
+            "steps": steps, "warmup": warmup, "ms_per_step": ms,
+            "tflops_per_gpu": (fwd + bwd) / (ms * 1e-3) / 1e12}
+
+
 def run(args) -> None:
     from bench import METRIC, UNIT, ClockSampler, _peaks
     from paper_2505_13211_b200.cp import CPAttention
@@ -104,6 +169,7 @@ def run(args) -> None:
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
 
     # e2e: host buffers in, gradients out, every step
+    o_h = torch.empty(L, HQ, D, dtype=torch.bfloat16).pin_memory()
     dq_h = torch.empty(L, HQ, D, dtype=torch.bfloat16).pin_memory()
     dk_h = torch.empty(L, HK, D, dtype=torch.bfloat16).pin_memory()
     dv_h = torch.empty(L, HK, D, dtype=torch.bfloat16).pin_memory()
@@ -139,6 +205,12 @@ def run(args) -> None:
             b = sets[i % 2]
             stream.wait_event(ev_qkv[i])
             out, lse, out32 = cpa.forward(b["q"], b["k"], b["v"])
+            ev_fwd = torch.cuda.Event()
+            ev_fwd.record(stream)
+            with torch.cuda.stream(d2h_s):  # O travels back while the backward computes
+                d2h_s.wait_event(ev_fwd)
+                o_h.copy_(out, non_blocking=True)
+                out.record_stream(d2h_s)
             stream.wait_event(ev_do[i])
             grads = cpa.backward(b["q"], b["k"], b["v"], out32, lse, b["do"])
             ev_done[i].record(stream)
@@ -168,6 +240,8 @@ def run(args) -> None:
     comm = torch.tensor([list(cpa.comm_tokens().values())], dtype=torch.float64, device=dev)
     dist.all_reduce(comm)
     if rank == 0:
+        cfg = config(world, mode)
+        assert cfg["flops_per_step"] == total, (cfg["flops_per_step"], total)
         peaks = _peaks()
         value = total / (ms.item() * 1e-3) / 1e12
         per_gpu = value / world
@@ -187,25 +261,17 @@ def run(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms.item(), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "cp_block_causal_magi1_24b", "seqlen": PER_RANK * world,
-                       "tokens_per_rank": PER_RANK, "num_heads_q": HQ, "num_heads_k": HK, "head_dim": D,
-                       "mask": f"block_causal(block={BLOCK})", "dispatch": "zigzag" if ring else ("contiguous" if uly else "greedy"),
-                       "cp_mode": mode,
-                       "dispatch_chunk_size": cpa.local_tokens if uly else cpa.chunk_size,
-                       "num_stages_fwd": world if ring else (1 if uly else cpa.xplan["num_stages_fwd"]),
-                       "num_stages_bwd": world if ring else (1 if uly else cpa.xplan["num_stages_bwd"]),
-                       "parallelism": f"cp{world}",
-                       "flops_per_step": total,
-                       "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),
-                       "comm_tokens_all_ranks": dict(zip(cpa.comm_tokens().keys(), comm[0].tolist())),
-                       "l2": "inputs larger than L2 per rank; no flush"},
+            "config": cfg,
+            "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),
+            "comm_tokens_all_ranks": dict(zip(cpa.comm_tokens().keys(), comm[0].tolist())),
             "roofline": {"bound": "tensor", "kernel": "whole CP step", "achieved": per_gpu,
                          "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": per_gpu / peaks["bf16"],
                          "traffic": None, "peak_source": peaks["source"]},
             "tflops_per_gpu": per_gpu,
             "e2e": {"value": total / (e2e_ms.item() * 1e-3) / 1e12, "unit": UNIT,
                     "h2d_bytes_per_step": sum(t.numel() * 2 for t in (q_h, k_h, v_h, do_h)),
-                    "d2h_bytes_per_step": sum(t.numel() * 2 for t in (dq_h, dk_h, dv_h)),
+                    "d2h_bytes_per_step": sum(t.numel() * 2 for t in (o_h, dq_h, dk_h, dv_h)),
+                    "copies": "H2D q, k, v, dO; D2H O, dQ, dK, dV (bf16), every step",
                     "ms_per_step": e2e_ms.item(), "per_rank": True},
             "clocks": clk,
             "gpu_launches": n_launch * args.steps,
