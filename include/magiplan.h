@@ -203,11 +203,14 @@ MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst,
                                                     void* cuda_stream);
 
 /* ---- diagnostics ------------------------------------------------------- */
-/* Event log of one forward / backward CTA (block index `block`) into a device
- * int64 buffer of 1 + 5 * 2 * 8000 entries: per warp role (MMA, two
- * elementwise warpgroups, TMA, load observer) 8000 {event << 32 | step,
- * globaltimer ns} pairs. NULL switches tracing off. Diagnostics only
- * (tools/trace_*.py). */
+/* Event log of one forward / backward CTA (block index `block`; a negative
+ * value -b-1 selects CTA b of the separate dQ pass) into a device int64 buffer
+ * of 1 + 5 * 2 * 8000 entries: per warp role (MMA, two elementwise
+ * warpgroups, TMA, load observer) 8000 {event << 32 | step, globaltimer ns}
+ * pairs. NULL switches tracing off. Only a library built with -DMAGI_TRACE
+ * (python -m paper_2505_13211_b200.build --trace) carries the traced kernel
+ * instantiations; the default build returns MAGIPLAN_ERR_USAGE for a non-NULL
+ * buffer. Diagnostics only (tools/trace_*.py). */
 MAGIPLAN_API magiplan_status magiplan_debug_set_trace(void* device_buffer, int32_t block);
 /* JSON-RPC access to individual planner functions for parity tests:
  * {"op": "slice_area" | "slice_area_in_cols" | "clip_slice" | "mask" |

@@ -9,10 +9,7 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-import os
-
-# MAGIPLAN_LIB: development A/B knob (load another build of the same ABI)
-_LIB_PATH = Path(os.environ.get("MAGIPLAN_LIB", Path(__file__).resolve().parent / "libmagiplan.so"))
+_LIB_PATH = Path(__file__).resolve().parent / "libmagiplan.so"
 
 OK, ERR_USAGE, ERR_CONSTRAINT, ERR_INTERNAL = 0, 2, 3, 4
 COUNT_MULTIPLICITY, COUNT_UNION = 0, 1

@@ -18,6 +18,11 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = ROOT / "build" / "obj"
+# diagnostics build (python -m paper_2505_13211_b200.build --trace): the
+# per-role event tracer of the FFA kernels (tools/trace_*.py) is compiled in
+# only with -DMAGI_TRACE; the default library carries one instantiation per
+# kernel and head_dim
+TRACE = "--trace" in sys.argv
 LIB = PKG / "libmagiplan.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -26,6 +31,9 @@ COMMON = [
     f"-I{ROOT / 'include'}", f"-I{ROOT / 'third_party'}", f"-I{CSRC}",
 ]
 CUDA_FLAGS = ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
+if TRACE:
+    COMMON.append("-DMAGI_TRACE")
+    OBJ = ROOT / "build" / "obj_trace"
 
 
 def _sources() -> list[Path]:

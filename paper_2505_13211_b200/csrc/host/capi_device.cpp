@@ -271,6 +271,11 @@ magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
 }
 
 magiplan_status magiplan_debug_set_trace(void* device_buffer, int32_t block) {
+#ifndef MAGI_TRACE
+  if (device_buffer != nullptr) {
+    return guarded([] { throw UsageError("tracing needs a library built with -DMAGI_TRACE"); });
+  }
+#endif
   magi::set_bwd_trace(static_cast<long long*>(device_buffer), block);
   magi::set_fwd_trace(static_cast<long long*>(device_buffer), block);
   return MAGIPLAN_OK;

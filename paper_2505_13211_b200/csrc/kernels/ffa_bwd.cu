@@ -25,7 +25,6 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
-#include <cstdlib>
 
 #include "ffa_common.cuh"
 #include "sm100.cuh"
@@ -63,11 +62,12 @@ struct BwdParams {
   int32_t lse_tma;      // lse / delta rows fetched by TMA (row stride 16B-aligned)
   long long* trace;     // diagnostics: event log of one CTA (nullptr = off)
   int32_t trace_block;
-  int32_t trace_kernel;  // 0: dK/dV kernel, 1: dQ kernel (MAGI_TRACE_DQ)
+  int32_t trace_kernel;  // 0: dK/dV kernel, 1: dQ kernel
 };
 
 long long* g_trace = nullptr;
 int g_trace_block = 0;
+int g_trace_kernel = 0;  // 0: dK/dV kernel, 1: dQ kernel
 
 __device__ __forceinline__ void store_row(void* base, size_t row_off, const uint32_t (&o)[32],
                                           int c, float scale, bool f32, bool accumulate) {
@@ -469,32 +469,12 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   cudaError_t err = cudaSuccess;
   if ((parts & 1) && num_k_tiles > 0) {
     const int smem = DkvSmem<D>::kBytes;  // 1024-aligned dynamic window, barriers inside
-    static const int poly = [] {
-      const char* e = std::getenv("MAGI_BWD_POLY");
-      return e ? std::atoi(e) : 0;
-    }();
-    static const int nw = [] {
-      const char* e = std::getenv("MAGI_DKV_WARPGROUPS");
-      return e && std::atoi(e) == 2 ? 2 : 4;
-    }();
-    // default 37.5% of the exponentials on the FMA pipe (measured best)
-    auto kern = poly == 4 ? ffa_bwd_dkdv_kernel<D, 0, false, 4>
-                          : (poly == 2 ? ffa_bwd_dkdv_kernel<D, 2, false, 4>
-                                       : (poly == 3 ? ffa_bwd_dkdv_kernel<D, 3, false, 4> : ffa_bwd_dkdv_kernel<D, 1, false, 4>));
-    int threads = DkvLayout<4>::kThreads;
-    if (nw == 2) {
-      kern = ffa_bwd_dkdv_kernel<D, 1, false, 2>;
-      threads = DkvLayout<2>::kThreads;
-    }
-    static const bool sched_y = [] {
-      const char* e = std::getenv("MAGI_DKV_SCHED");
-      return e != nullptr && std::atoi(e) == 1;
-    }();
-    if (sched_y) kern = nw == 2 ? ffa_bwd_dkdv_kernel<D, 1, false, 2, true> : ffa_bwd_dkdv_kernel<D, 1, false, 4, true>;
-    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, 4>;  // diagnostics
-    if (prm.trace != nullptr && prm.trace_kernel == 0 && nw == 2) kern = ffa_bwd_dkdv_kernel<D, 1, true, 2>;
-    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem);
+    // 37.5% of the exponentials on the FMA pipe, four elementwise warpgroups
+    auto kern = ffa_bwd_dkdv_kernel<D, 1, false, 4>;
+#ifdef MAGI_TRACE
+    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, 4>;
+#endif
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
     BwdParams pk = prm;
     pk.lse_tma = (prm.seqlen_q % 4) == 0;
@@ -503,26 +483,19 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
       td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
     }
-    kern<<<dim3(num_k_tiles * prm.hk), threads, smem, stream>>>(tq, tk, tv, tdo, tl,
-                                                                                   td, pk);
+    kern<<<dim3(num_k_tiles * prm.hk), DkvLayout<4>::kThreads, smem, stream>>>(tq, tk, tv, tdo, tl, td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
   if ((parts & 2) && num_q_tiles > 0) {
     const int smem = DqSmem<D>::kBytes + 1024;
-    static const int dq_poly = [] {
-      const char* e = std::getenv("MAGI_DQ_POLY");
-      return e ? std::atoi(e) : 1;
-    }();
-    auto dq_kern = dq_poly == 0 ? ffa_bwd_dq_kernel<D, false, 0>
-                                : (dq_poly == 2 ? ffa_bwd_dq_kernel<D, false, 2>
-                                                : (dq_poly == 3 ? ffa_bwd_dq_kernel<D, false, 3> : ffa_bwd_dq_kernel<D, false, 1>));
+    auto dq_kern = ffa_bwd_dq_kernel<D, false, 1>;  // 37.5% of the exponentials on the FMA pipe
+#ifdef MAGI_TRACE
     if (prm.trace != nullptr && prm.trace_kernel == 1) dq_kern = ffa_bwd_dq_kernel<D, true, 1>;
-    err = cudaFuncSetAttribute(dq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               smem);
+#endif
+    err = cudaFuncSetAttribute(dq_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
-    dq_kern<<<dim3(num_q_tiles * prm.hq), kThreads, smem, stream>>>(tq, tk, tv, tdo,
-                                                                                 prm);
+    dq_kern<<<dim3(num_q_tiles * prm.hq), kThreads, smem, stream>>>(tq, tk, tv, tdo, prm);
     err = cudaGetLastError();
   }
   return err;
@@ -558,11 +531,7 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
   prm.num_q_tiles = num_q_tiles;
   prm.trace = g_trace;
   prm.trace_block = g_trace_block;
-  static const bool trace_dq = [] {
-    const char* e = std::getenv("MAGI_TRACE_DQ");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  prm.trace_kernel = trace_dq ? 1 : 0;
+  prm.trace_kernel = g_trace_kernel;
   prm.dout = grad_out;
   prm.grad_f32 = grad_f32;
   prm.accumulate = accumulate;
@@ -578,6 +547,7 @@ namespace magi {
 // (int64: [0] unused, then per-role {event << 32 | step, ns} regions); nullptr = off.
 void set_bwd_trace(long long* buffer, int block) {
   g_trace = buffer;
-  g_trace_block = block;
+  g_trace_block = block < 0 ? -block - 1 : block;
+  g_trace_kernel = block < 0 ? 1 : 0;  // a negative block index selects the dQ kernel
 }
 }  // namespace magi

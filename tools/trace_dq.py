@@ -1,4 +1,6 @@
-"""Timeline of one dQ CTA (diagnostics; MAGI_TRACE_DQ=1 + magiplan_debug_set_trace).
+"""Timeline of one dQ CTA (diagnostics: a library built with
+`python -m paper_2505_13211_b200.build --trace`; magiplan_debug_set_trace with
+a negative block index -b-1 selects dQ CTA b).
 
 MMA 1 = S slot free (S(t) in registers), 2 = dS(t) ready (p_full), 3 = dP(t+1)
 issued; warpgroups 10 = S(t) ready, 11 = exponentials done, 12 = dP(t) ready,
@@ -8,7 +10,6 @@ import os
 import statistics
 import sys
 
-os.environ["MAGI_TRACE_DQ"] = "1"
 import torch  # noqa: E402
 
 sys.path.insert(0, ".")
@@ -30,7 +31,7 @@ def main(block: int = 0):
     out, lse = ffa_forward(plan, q, k, v)
     ffa_backward(plan, q, k, v, out, lse, do)
     buf = torch.zeros(1 + 5 * 2 * CAP, dtype=torch.int64, device="cuda")
-    _lib.check(_lib.lib().magiplan_debug_set_trace(buf.data_ptr(), block))
+    _lib.check(_lib.lib().magiplan_debug_set_trace(buf.data_ptr(), -block - 1))
     ffa_backward(plan, q, k, v, out, lse, do)
     torch.cuda.synchronize()
     _lib.check(_lib.lib().magiplan_debug_set_trace(None, 0))
