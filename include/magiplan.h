@@ -163,6 +163,17 @@ MAGIPLAN_API magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, con
                                               float softmax_scale, int32_t grad_dtype,
                                               int32_t accumulate, void* cuda_stream);
 
+/* The backward of one context-parallel stage (f32 buffers): dQ is ADDED to
+ * grad_q (the running dQ of the earlier stages), while grad_k / grad_v
+ * receive the stage's fresh partial dK / dV of the received keys (written,
+ * not added; keys no slice reaches get zeros). */
+MAGIPLAN_API magiplan_status magiplan_ffa_bwd_stage(const magiplan_ffa_plan* plan, const void* q,
+                                                    const void* k, const void* v, const float* lse,
+                                                    const float* delta, const void* grad_out,
+                                                    float* grad_q, float* grad_k, float* grad_v,
+                                                    int64_t num_heads_q, int64_t num_heads_k,
+                                                    float softmax_scale, void* cuda_stream);
+
 /* The two halves of magiplan_ffa_bwd, for per-kernel timing and for running
  * them on separate streams: the k-major dK/dV pass and the q-major dQ pass. */
 MAGIPLAN_API magiplan_status magiplan_ffa_bwd_dkdv(const magiplan_ffa_plan* plan, const void* q,

@@ -44,6 +44,7 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_ffa_fwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_ffa_bwd_preprocess": (C.c_int, [_vp, _vp, _vp, _i64, _i64, _i32, _i32, _vp]),
     "magiplan_ffa_bwd": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
+    "magiplan_ffa_bwd_stage": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp]),
     "magiplan_ffa_bwd_dkdv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_ffa_bwd_dq": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_range_gather": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),

@@ -342,16 +342,12 @@ class CPAttention:
             dvb = torch.empty_like(dkb)
             e0 = self._ev(cur)
             if st.plan is not None:
-                # dK/dV of the received keys (fresh partials), then dQ added
-                # into the running dQ of the earlier stages
-                _lib.check(Ld.magiplan_ffa_bwd_dkdv(st.plan.handle, q.data_ptr(), kb.data_ptr(),
-                                                    vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
-                                                    dout.data_ptr(), dkb.data_ptr(), dvb.data_ptr(),
-                                                    self.hq, self.hk, self.scale, _lib.F32, 0, sp))
-                _lib.check(Ld.magiplan_ffa_bwd_dq(st.plan.handle, q.data_ptr(), kb.data_ptr(),
-                                                  vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
-                                                  dout.data_ptr(), dq.data_ptr(), self.hq, self.hk,
-                                                  self.scale, _lib.F32, 1, sp))
+                # fresh partial dK/dV of the received keys; dQ added into the
+                # running dQ of the earlier stages
+                _lib.check(Ld.magiplan_ffa_bwd_stage(st.plan.handle, q.data_ptr(), kb.data_ptr(),
+                                                     vb.data_ptr(), lse.data_ptr(), delta.data_ptr(),
+                                                     dout.data_ptr(), dq.data_ptr(), dkb.data_ptr(),
+                                                     dvb.data_ptr(), self.hq, self.hk, self.scale, sp))
             else:
                 dkb.zero_()
                 dvb.zero_()

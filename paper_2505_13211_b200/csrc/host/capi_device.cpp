@@ -211,6 +211,22 @@ magiplan_status magiplan_ffa_bwd(const magiplan_ffa_plan* plan, const void* q, c
                        num_heads_k, softmax_scale, grad_dtype, accumulate, 3, cuda_stream);
 }
 
+magiplan_status magiplan_ffa_bwd_stage(const magiplan_ffa_plan* plan, const void* q, const void* k,
+                                       const void* v, const float* lse, const float* delta,
+                                       const void* grad_out, float* grad_q, float* grad_k,
+                                       float* grad_v, int64_t num_heads_q, int64_t num_heads_k,
+                                       float softmax_scale, void* cuda_stream) {
+  MAGI_REQUIRE(plan && q && k && v && lse && delta && grad_out && grad_q && grad_k && grad_v);
+  // the k-major pass writes the stage's fresh partial dK / dV, the q-major
+  // pass adds the stage's dQ into the running dQ
+  const magiplan_status st =
+      ffa_bwd_parts(plan, q, k, v, lse, delta, grad_out, grad_k, grad_k, grad_v, num_heads_q, num_heads_k,
+                    softmax_scale, MAGIPLAN_F32, 0, 1, cuda_stream);
+  if (st != MAGIPLAN_OK) return st;
+  return ffa_bwd_parts(plan, q, k, v, lse, delta, grad_out, grad_q, grad_q, grad_q, num_heads_q, num_heads_k,
+                       softmax_scale, MAGIPLAN_F32, 1, 2, cuda_stream);
+}
+
 magiplan_status magiplan_ffa_bwd_dkdv(const magiplan_ffa_plan* plan, const void* q,
                                       const void* k, const void* v, const float* lse,
                                       const float* delta, const void* grad_out, void* grad_k,

@@ -117,12 +117,9 @@ def stage_overhead_us(dev, S: int = 131072, block: int = 8192, pieces: int = 4) 
     scale = D ** -0.5
 
     def bwd_calls(pl, kk, vv, dkk, dvv):
-        _lib.check(L.magiplan_ffa_bwd_dq(pl.handle, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), lse2.data_ptr(),
-                                         delta.data_ptr(), do.data_ptr(), dq.data_ptr(), HQ, HK, scale,
-                                         _lib.F32, 1, sp))
-        _lib.check(L.magiplan_ffa_bwd_dkdv(pl.handle, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), lse2.data_ptr(),
-                                           delta.data_ptr(), do.data_ptr(), dkk.data_ptr(), dvv.data_ptr(), HQ,
-                                           HK, scale, _lib.F32, 0, sp))
+        _lib.check(L.magiplan_ffa_bwd_stage(pl.handle, q.data_ptr(), kk.data_ptr(), vv.data_ptr(), lse2.data_ptr(),
+                                            delta.data_ptr(), do.data_ptr(), dq.data_ptr(), dkk.data_ptr(),
+                                            dvv.data_ptr(), HQ, HK, scale, sp))
 
     def bwd_whole():
         bwd_calls(whole, k, v, dk, dv)

@@ -51,6 +51,18 @@ __global__ void __launch_bounds__(128, 1) tile_kernel(float* acc, int mode, int 
     } else if (mode == 1) {
 #pragma unroll 4
       for (int r = warp; r < 128; r += 4) red_v4(base + static_cast<size_t>(r) * HQ * D + 4 * lane, v);
+    } else if (mode == 4) {
+      // 8 rows x 64 B per warp instruction (lane/4 = row, 4 lanes x 16 B per row)
+      for (int r0 = warp * 32; r0 < warp * 32 + 32; r0 += 8)
+#pragma unroll
+        for (int c = 0; c < 128; c += 16)
+          red_v4(base + static_cast<size_t>(r0 + lane / 4) * HQ * D + c + 4 * (lane % 4), v);
+    } else if (mode == 5) {
+      // 4 rows x 128 B per warp instruction (lane/8 = row, 8 lanes x 16 B per row)
+      for (int r0 = warp * 32; r0 < warp * 32 + 32; r0 += 4)
+#pragma unroll
+        for (int c = 0; c < 128; c += 32)
+          red_v4(base + static_cast<size_t>(r0 + lane / 8) * HQ * D + c + 4 * (lane % 8), v);
     } else if (mode == 2) {
       // one thread per row issues a 512B bulk reduce
       float* row = base + static_cast<size_t>(tid) * HQ * D;
@@ -126,9 +138,9 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const char* names[] = {"red.v4 thread=row", "red.v4 coalesced rows", "bulk reduce 512B rows",
-                         "ld.v4 thread=row"};
+                         "ld.v4 thread=row", "red.v4 8 rows x 64B", "red.v4 4 rows x 128B"};
   for (int grid : {148}) {
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 6; ++mode) {
       const int steps = 256;
       for (int rep = 0; rep < 2; ++rep) {
         cudaEventRecord(a);
