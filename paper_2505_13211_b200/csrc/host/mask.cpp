@@ -325,7 +325,8 @@ AttnMask build_pattern(const PatternSpec& spec) {
         m.slices.push_back({{0, s}, {0, s}, SliceType::Causal});
       } else {
         m.slices.push_back({{0, w}, {0, w}, SliceType::Causal});
-        // rows q >= w see exactly [q - w + 1, q]: a width-w diagonal band
+        // later rows: BI_CAUSAL over keys [1, s) anchors both bounds on the
+        // diagonal, so row q keeps the last w keys up to itself
         m.slices.push_back({{w, s}, {1, s}, SliceType::BiCausal});
       }
       break;
