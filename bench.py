@@ -464,11 +464,12 @@ def run_single(args) -> None:
     dom = max((n for n, _, fl in parts if fl), key=lambda n: per_part[n])
     dom_fl = dict((n, fl) for n, _, fl in parts)[dom]
     achieved = dom_fl / (per_part[dom] * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_tag = None, None
     summ = ROOT / "profiles" / "ncu_summary.json"
     if summ.exists():
         try:
-            traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch", {}).get(dom)
+            js = json.loads(summ.read_text())
+            traffic, traffic_tag = js.get("dram_bytes_per_launch", {}).get(dom), js.get("tag")
         except Exception:  # noqa: BLE001
             traffic = None
     line = {
@@ -478,6 +479,7 @@ def run_single(args) -> None:
         "config": config,
         "roofline": {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peaks["bf16"],
                      "unit": "TFLOP/s", "frac": achieved / peaks["bf16"], "traffic": traffic,
+                     "traffic_source": f"ncu --set full, profiles/ncu_{traffic_tag}.md" if traffic_tag else None,
                      "peak_source": peaks["source"], "peak_sustained": peaks["bf16_sustained"],
                      "step_frac": value / peaks["bf16"]},
         "kernels": kernels,
