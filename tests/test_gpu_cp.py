@@ -81,6 +81,11 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode, stages, check
         idx = cpa.local_token_index()
         q, k, v, do = (t[idx.to(t.device)].contiguous().to(dev) for t in (Q, K, V, DO))
         out, lse, out32 = cpa.forward(q, k, v)
+        if mode == "ulysses":
+            # another forward in between (micro-batches / recompute): the
+            # backward of the first must not pick up the second's activations
+            q2 = (q.float() * 0.5).to(torch.bfloat16)
+            cpa.forward(q2, k, v)
         dq, dk, dv = cpa.backward(q, k, v, out32, lse, do)
         # a second pass reuses the cached plans and buffers: same bits
         out_b, lse_b, out32_b = cpa.forward(q, k, v)

@@ -86,3 +86,57 @@ def test_autograd_function(built_lib, cuda):
     torch.cuda.synchronize()
     assert q.grad is not None and k.grad.shape == k.shape and v.grad.dtype == torch.bfloat16
     assert torch.isfinite(q.grad.float()).all()
+
+
+def test_stage_backward_and_prepare(built_lib, cuda):
+    """magiplan_ffa_bwd_stage (the CP stage backward): dQ is added into the
+    running dQ, dK/dV are the stage's fresh partials (overwritten, keys no
+    slice reaches -> 0); a prepared plan gives the same bits."""
+    import math
+
+    from paper_2505_13211_b200 import _lib
+    from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward
+
+    sq, sk, hq, hk, d, qr, kr, ty = CASES["uncovered_keys"]
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=8)
+    plan = FFAPlan(qr, kr, ty, sq, sk, d)
+    plan.prepare()
+    out, lse = ffa_forward(plan, q, k, v, out_dtype=torch.float32)
+    dq0, dk0, dv0 = ffa_backward(plan, q, k, v, out, lse, do, grad_dtype=torch.float32)
+    delta = (do.float() * out).sum(-1).t().contiguous()
+    run = torch.randn(sq, hq, d, device=cuda)  # running dQ of earlier stages
+    dq = run.clone()
+    dk = torch.full((sk, hk, d), 7.0, device=cuda)  # garbage: must be overwritten
+    dv = torch.full_like(dk, -3.0)
+    L = _lib.lib()
+    _lib.check(L.magiplan_ffa_bwd_stage(plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(),
+                                        delta.data_ptr(), do.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                                        dv.data_ptr(), hq, hk, 1.0 / math.sqrt(d),
+                                        torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.allclose(dq, run + dq0, rtol=1e-5, atol=1e-5)
+    assert torch.equal(dk, dk0) and torch.equal(dv, dv0)
+
+
+def test_buffer_validation(built_lib, cuda):
+    """Caller buffers are checked before any device write: wrong shape,
+    dtype, layout or device is a ValueError."""
+    from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward
+
+    sq, sk, hq, hk, d, qr, kr, ty = CASES["varlen_mixed"]
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=9)
+    plan = FFAPlan(qr, kr, ty, sq, sk, d)
+    with pytest.raises(ValueError):
+        ffa_forward(plan, q, k, v, out=torch.empty(sq, hq, d + 1, device=cuda, dtype=torch.bfloat16))
+    with pytest.raises(ValueError):
+        ffa_forward(plan, q, k, v, lse=torch.empty(hq, sq, device=cuda, dtype=torch.bfloat16))
+    with pytest.raises(ValueError):
+        ffa_forward(plan, q, k, v, out=torch.empty(hq, sq, d, device=cuda, dtype=torch.bfloat16).transpose(0, 1))
+    out, lse = ffa_forward(plan, q, k, v)
+    with pytest.raises(ValueError):
+        ffa_backward(plan, q, k, v, out, lse, do, dq=torch.empty(sq, hq, d, device=cuda, dtype=torch.float16))
+    with pytest.raises(ValueError):
+        ffa_backward(plan, q, k, v, out, lse, do, dq=torch.empty(sq, hq, d, device=cuda),
+                     dk=torch.empty(sk, hk, d, device=cuda, dtype=torch.bfloat16))
+    with pytest.raises(ValueError):
+        ffa_backward(plan, q, k, v, out, lse, do.float())
