@@ -213,6 +213,37 @@ MAGIPLAN_API magiplan_status magiplan_range_scatter_add_f32(const float* src, fl
 MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
                                                     void* cuda_stream);
 
+/* ---- context-parallel executor (new) ------------------------------------ */
+/* The planner's multi-stage CP schedule run on this process's GPU (one
+ * process per GPU): GroupCast / GroupReduce over NCCL point-to-point
+ * (resolved at run time from libnccl.so.2) on two communicators and two
+ * high-priority streams, FFA stages with the LSE merge, deterministic
+ * per-source scatter-add of the partial dK / dV. Same schedule as
+ * paper_2505_13211_b200/cp.py. */
+typedef struct magiplan_cp magiplan_cp;
+/* 128 bytes (ncclUniqueId) made once (e.g. on rank 0) and handed to every rank. */
+MAGIPLAN_API magiplan_status magiplan_cp_unique_id(void* out_id);
+/* Collective over the scenario's cp_size ranks (each calls it with its rank
+ * on its current CUDA device). */
+MAGIPLAN_API magiplan_status magiplan_cp_create(const magiplan_scenario* scenario, int32_t rank,
+                                                const void* nccl_unique_id, int64_t num_heads_q,
+                                                int64_t num_heads_k, int32_t head_dim,
+                                                float softmax_scale, magiplan_cp** out);
+MAGIPLAN_API void magiplan_cp_free(magiplan_cp* cp);
+/* {"rank","cp_size","local_tokens","chunk_size","chunks":[global chunk ids in
+ *  local order],"num_stages_fwd","num_stages_bwd","area_multiplicity"} */
+MAGIPLAN_API magiplan_status magiplan_cp_describe(const magiplan_cp* cp, char** out_json);
+/* Local shards in chunk order: q [L, hq, d], k / v [L, hk, d] bf16; out_f32
+ * [L, hq, d] and lse [hq, L] f32 (kept for the backward); out_bf16 optional. */
+MAGIPLAN_API magiplan_status magiplan_cp_forward(magiplan_cp* cp, const void* q, const void* k,
+                                                 const void* v, float* out_f32, float* lse,
+                                                 void* out_bf16, void* cuda_stream);
+/* dq [L, hq, d], dk / dv [L, hk, d] bf16 of the local shard. */
+MAGIPLAN_API magiplan_status magiplan_cp_backward(magiplan_cp* cp, const void* q, const void* k,
+                                                  const void* v, const float* out_f32,
+                                                  const float* lse, const void* dout, void* dq,
+                                                  void* dk, void* dv, void* cuda_stream);
+
 /* ---- diagnostics ------------------------------------------------------- */
 /* Event log of one forward / backward CTA (block index `block`; a negative
  * value -b-1 selects CTA b of the separate dQ pass) into a device int64 buffer

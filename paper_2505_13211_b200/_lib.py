@@ -47,6 +47,12 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_ffa_bwd_stage": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _vp]),
     "magiplan_ffa_bwd_dkdv": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_ffa_bwd_dq": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
+    "magiplan_cp_unique_id": (C.c_int, [_vp]),
+    "magiplan_cp_create": (C.c_int, [_vp, _i32, _vp, _i64, _i64, _i32, _f32, C.POINTER(_vp)]),
+    "magiplan_cp_free": (None, [_vp]),
+    "magiplan_cp_describe": (C.c_int, [_vp, C.POINTER(_vp)]),
+    "magiplan_cp_forward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "magiplan_cp_backward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "magiplan_range_gather": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "magiplan_range_scatter_add_f32": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "magiplan_cast_f32_bf16": (C.c_int, [_vp, _vp, _i64, _vp]),

@@ -379,3 +379,80 @@ class CPAttention:
         return {"fwd_cast_recv_tokens": cast,
                 "bwd_cast_recv_tokens": sum(sum(st.recv_splits) for st in self.bwd_stages),
                 "bwd_reduce_recv_tokens": sum(sum(st.send_splits) for st in self.bwd_stages)}
+
+
+class CPExecutorC:
+    """The same schedule through the C ABI's own executor (magiplan_cp_*,
+    csrc/host/cp_exec.cpp): what a C / C++ consumer of libmagiplan.so runs.
+    Torch only provides device memory, the stream and the NCCL unique-id
+    broadcast; the executor creates its own NCCL communicators."""
+
+    def __init__(self, scenario: dict | str, num_heads_q: int, num_heads_k: int, head_dim: int,
+                 group=None, device=None, softmax_scale: float | None = None):
+        import ctypes as C
+
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.hq, self.hk, self.d = num_heads_q, num_heads_k, head_dim
+        self.scale = 1.0 / math.sqrt(head_dim) if softmax_scale is None else softmax_scale
+        self.L = _lib.lib()
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            _lib.check(self.L.magiplan_cp_unique_id(uid))
+        obj = [bytes(uid.raw)]
+        if self.world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        uid = C.create_string_buffer(obj[0], 128)
+        self._scen = Scenario(scenario)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _lib.check(self.L.magiplan_cp_create(self._scen._h, self.rank, uid, num_heads_q, num_heads_k, head_dim,
+                                                 self.scale, C.byref(h)))
+        self._h = h
+        out = C.c_void_p()
+        _lib.check(self.L.magiplan_cp_describe(self._h, C.byref(out)))
+        info = json.loads(_lib.take_string(out))
+        self.chunks, self.chunk_size = info["chunks"], info["chunk_size"]
+        self.local_tokens = info["local_tokens"]
+        self.xplan = {"num_stages_fwd": info["num_stages_fwd"], "num_stages_bwd": info["num_stages_bwd"],
+                      "area_multiplicity": info["area_multiplicity"], "seqlen": self.local_tokens * self.world}
+
+    def local_token_index(self) -> torch.Tensor:
+        cs = self.chunk_size
+        idx = [torch.arange(c * cs, (c + 1) * cs) for c in self.chunks]
+        return torch.cat(idx) if idx else torch.empty(0, dtype=torch.int64)
+
+    def forward(self, q, k, v):
+        L = self.local_tokens
+        out32 = torch.empty((L, self.hq, self.d), dtype=torch.float32, device=q.device)
+        lse = torch.empty((self.hq, L), dtype=torch.float32, device=q.device)
+        out = torch.empty((L, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
+        _lib.check(self.L.magiplan_cp_forward(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out32.data_ptr(),
+                                              lse.data_ptr(), out.data_ptr(),
+                                              torch.cuda.current_stream(q.device).cuda_stream))
+        return out, lse, out32
+
+    def backward(self, q, k, v, out_f32, lse, dout):
+        dq = torch.empty_like(q)
+        dk, dv = torch.empty_like(k), torch.empty_like(v)
+        _lib.check(self.L.magiplan_cp_backward(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(), out_f32.data_ptr(),
+                                               lse.data_ptr(), dout.data_ptr(), dq.data_ptr(), dk.data_ptr(),
+                                               dv.data_ptr(), torch.cuda.current_stream(q.device).cuda_stream))
+        return dq, dk, dv
+
+    def flops(self) -> tuple[int, int]:
+        fwd = 4 * int(self.xplan["area_multiplicity"]) * self.hq * self.d
+        return fwd, fwd * 5 // 2
+
+    def comm_tokens(self) -> dict:
+        return {}
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                torch.cuda.synchronize(self.device)
+                self.L.magiplan_cp_free(h)
+            except Exception:  # noqa: BLE001
+                pass

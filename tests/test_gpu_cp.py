@@ -73,6 +73,12 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode, stages, check
         elif mode == "ring":
             cpa = RingAttention(mask, hq, hk, d)
             S = cpa.chunk_size * 2 * world
+        elif mode == "capi":  # the C-ABI executor (csrc/host/cp_exec.cpp)
+            from paper_2505_13211_b200.cp import CPExecutorC
+
+            cpa = CPExecutorC(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d)
+            S = cpa.xplan["seqlen"]
+            nst = (cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"])
         else:
             cpa = CPAttention(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d)
             S = cpa.xplan["seqlen"]
@@ -153,6 +159,10 @@ CASES = [
     ("magi", BC4096, 256, 3),
     ("magi", VARLEN, 128, 4),
     ("magi", CAUSAL, 192, 2),
+    # the same schedule through the C ABI's executor (no Python in the loop)
+    ("capi", BC4096, 256, 3),
+    ("capi", VARLEN, 128, 4),
+    ("capi", CAUSAL, 192, None),
     # ring-attention baseline (zigzag dispatch, K/V around the ring)
     ("ring", BC4096, 0, None),
     ("ring", {"seqlen": 4096, "pattern": "causal"}, 0, None),
