@@ -135,6 +135,10 @@ def run(args) -> None:
         from paper_2505_13211_b200.ulysses import UlyssesAttention
 
         cpa = UlyssesAttention(scenario(world)["workload"]["mask"], HQ, HK, D)
+    elif mode == "capi":
+        from paper_2505_13211_b200.cp import CPExecutorC
+
+        cpa = CPExecutorC(scenario(world), HQ, HK, D)
     else:
         cpa = CPAttention(scenario(world), HQ, HK, D)
     L = cpa.local_tokens
@@ -237,7 +241,8 @@ def run(args) -> None:
 
     fwd, bwd = cpa.flops()
     total = fwd + bwd
-    comm = torch.tensor([list(cpa.comm_tokens().values())], dtype=torch.float64, device=dev)
+    comm_keys = list(cpa.comm_tokens().keys())
+    comm = torch.tensor([list(cpa.comm_tokens().values()) or [0.0]], dtype=torch.float64, device=dev)
     dist.all_reduce(comm)
     if rank == 0:
         cfg = config(world, mode)
@@ -251,6 +256,11 @@ def run(args) -> None:
         elif ring:
             n_plans = sum(p is not None for p in cpa.plans)
             n_launch = n_plans * 3 + 1 + 1 + 3  # fwd + dq + dkdv per plan, cast, preprocess, final casts
+        elif mode == "capi":
+            nf, nb = cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"]
+            # host fwd + per stage (gather x2, ffa), cast; preprocess, host bwd (2), per stage
+            # (gather x2, dkdv, dq, scatter-adds), final casts
+            n_launch = 2 + 3 * nf + 1 + 3 + 4 * nb + 2 * world * nb + 3
         else:
             for st in cpa.fwd_stages:
                 n_launch += 1 + 2 * (1 if sum(st.send_splits) else 0)
@@ -263,7 +273,7 @@ def run(args) -> None:
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": cfg,
             "tokens_per_s": PER_RANK * world / (ms.item() * 1e-3),
-            "comm_tokens_all_ranks": dict(zip(cpa.comm_tokens().keys(), comm[0].tolist())),
+            "comm_tokens_all_ranks": dict(zip(comm_keys, comm[0].tolist())),
             "roofline": {"bound": "tensor", "kernel": "whole CP step", "achieved": per_gpu,
                          "peak": peaks["bf16"], "unit": "TFLOP/s", "frac": per_gpu / peaks["bf16"],
                          "traffic": None, "peak_source": peaks["source"]},
