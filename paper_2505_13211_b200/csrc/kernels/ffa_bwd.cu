@@ -470,12 +470,9 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
   if ((parts & 1) && num_k_tiles > 0) {
     const int smem = DkvSmem<D>::kBytes;  // 1024-aligned dynamic window, barriers inside
     // 37.5% of the exponentials on the FMA pipe, four elementwise warpgroups
-#ifndef MAGI_DKV_NW
-#define MAGI_DKV_NW 4
-#endif
-    auto kern = ffa_bwd_dkdv_kernel<D, 1, false, MAGI_DKV_NW>;
+    auto kern = ffa_bwd_dkdv_kernel<D, 1, false, 4>;
 #ifdef MAGI_TRACE
-    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, MAGI_DKV_NW>;
+    if (prm.trace != nullptr && prm.trace_kernel == 0) kern = ffa_bwd_dkdv_kernel<D, 1, true, 4>;
 #endif
     err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (err != cudaSuccess) return err;
@@ -486,7 +483,7 @@ cudaError_t launch_bwd_impl(const BwdParams& prm, int num_q_tiles, int num_k_til
       tl = make_tmap_f32_rows(prm.lse, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
       td = make_tmap_f32_rows(prm.delta, static_cast<uint64_t>(prm.hq), static_cast<uint64_t>(prm.seqlen_q), 128);
     }
-    kern<<<dim3(num_k_tiles * prm.hk), DkvLayout<MAGI_DKV_NW>::kThreads, smem, stream>>>(tq, tk, tv, tdo, tl, td, pk);
+    kern<<<dim3(num_k_tiles * prm.hk), DkvLayout<4>::kThreads, smem, stream>>>(tq, tk, tv, tdo, tl, td, pk);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
