@@ -31,9 +31,10 @@ COMMON = [
     f"-I{ROOT / 'include'}", f"-I{ROOT / 'third_party'}", f"-I{CSRC}",
 ]
 CUDA_FLAGS = ["-Xptxas", "-v", "--expt-relaxed-constexpr"]
-if TRACE:
+if TRACE:  # separate objects and library: never replaces the product build
     COMMON.append("-DMAGI_TRACE")
     OBJ = ROOT / "build" / "obj_trace"
+    LIB = ROOT / "build" / "trace" / "libmagiplan.so"
 
 
 def _sources() -> list[Path]:
@@ -71,6 +72,7 @@ def build(verbose: bool = False) -> Path:
     if LIB.exists() and LIB.stat().st_mtime >= newest:
         return LIB  # up to date (e.g. the prebuilt library shipped to a GPU box)
     OBJ.mkdir(parents=True, exist_ok=True)
+    LIB.parent.mkdir(parents=True, exist_ok=True)
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         results = list(ex.map(lambda s: _compile(s, hdr_mtime, verbose), srcs))
     objs = [o for o, _ in results]

@@ -4,6 +4,7 @@ Per-role logs (globaltimer ns): MMA 1 = P^T(t) ready, 2 = Q(t+1) landed,
 3 = dS^T(t) ready, 4 = dO(t+1) landed; warpgroups 10..13 = S(t) ready, P^T
 written, dP(t) ready, dS^T(t) written; TMA 30 / 31 = Q / dO slot for step t free.
 """
+import os
 import statistics
 import sys
 
@@ -11,6 +12,9 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2505_13211_b200 import _lib  # noqa: E402
+
+# the diagnostics build (python -m paper_2505_13211_b200.build --trace), or MAGI_LIB
+_lib._LIB_PATH = _lib.Path(os.environ.get("MAGI_LIB", "build/trace/libmagiplan.so")).resolve()
 from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward  # noqa: E402
 
 CAP = 8000

@@ -14,6 +14,9 @@ import torch  # noqa: E402
 
 sys.path.insert(0, ".")
 from paper_2505_13211_b200 import _lib  # noqa: E402
+
+# the diagnostics build (python -m paper_2505_13211_b200.build --trace), or MAGI_LIB
+_lib._LIB_PATH = _lib.Path(os.environ.get("MAGI_LIB", "build/trace/libmagiplan.so")).resolve()
 from paper_2505_13211_b200.ffa import FFAPlan, ffa_backward, ffa_forward  # noqa: E402
 
 CAP = 8000
