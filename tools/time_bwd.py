@@ -1,10 +1,10 @@
-"""Development timing of the FFA passes at config 2 (S = 32768, block-causal
-4096, 24 q / 8 kv heads, d = 128) for one build of the library:
+"""Development timing of the FFA passes for one build of the library:
 
-    python tools/time_bwd.py [path/to/libmagiplan.so]
+    python tools/time_bwd.py [path/to/libmagiplan.so] [workload]
 
-prints ms per call of the forward, the fused backward (dQ, dK, dV) and the
-dK/dV-only backward."""
+workload: a bench.py WORKLOADS key (default config 2: S = 32768, block-causal
+4096, 24 q / 8 kv heads, d = 128). Prints ms per call of the forward, the
+whole backward (dQ, dK, dV), the dK/dV pass and the dQ pass."""
 import json
 import math
 import sys
@@ -12,17 +12,25 @@ from pathlib import Path
 
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
 from paper_2505_13211_b200 import _lib  # noqa: E402
 
 if len(sys.argv) > 1:
     _lib._LIB_PATH = Path(sys.argv[1]).resolve()
+import bench  # noqa: E402
 from paper_2505_13211_b200.ffa import FFAPlan  # noqa: E402
 
-S, HQ, HK, D, B = 32768, 24, 8, 128, 4096
-qr = [[i, i + B] for i in range(0, S, B)]
-kr = [[0, i + B] for i in range(0, S, B)]
-plan = FFAPlan(qr, kr, [0] * len(qr), S, S, D)
+WL = sys.argv[2] if len(sys.argv) > 2 else bench.DEFAULT_WORKLOAD
+W = bench.WORKLOADS[WL]
+S, HQ, HK, D, B = W["seqlen"], W["hq"], W["hk"], W["d"], W["block"]
+if W.get("varlen"):
+    qr, kr, ty = bench.varlen_packed(S)
+else:
+    qr = [[i, i + B] for i in range(0, S, B)]
+    kr = [[0, i + B] for i in range(0, S, B)]
+    ty = [0] * len(qr)
+plan = FFAPlan(qr, kr, ty, S, S, D)
 dev = torch.device("cuda", 0)
 q = torch.randn(S, HQ, D, device=dev, dtype=torch.bfloat16)
 k = torch.randn(S, HK, D, device=dev, dtype=torch.bfloat16)
@@ -61,11 +69,12 @@ def t(fn, n=5):
     return e0.elapsed_time(e1) / n
 
 
-area = 8 * 9 // 2 * B * B
+area = plan.describe()["area_multiplicity"]
 dqo = lambda: _lib.check(L.magiplan_ffa_bwd_dq(plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(),  # noqa: E731
                                                 lse.data_ptr(), delta.data_ptr(), do.data_ptr(), dq.data_ptr(),
                                                 HQ, HK, sc, BF, 0, sp))
-res = {"lib": str(_lib._LIB_PATH), "fwd_ms": t(fwd), "bwd_ms": t(bwd), "dkdv_only_ms": t(dkdv),
+res = {"lib": str(_lib._LIB_PATH), "workload": WL, "fwd_ms": t(fwd), "bwd_ms": t(bwd), "dkdv_only_ms": t(dkdv),
        "dq_only_ms": t(dqo)}
+res["fwd_tflops"] = 4 * area * HQ * D / res["fwd_ms"] / 1e9
 res["bwd_tflops"] = 10 * area * HQ * D / res["bwd_ms"] / 1e9
 print(json.dumps(res))
