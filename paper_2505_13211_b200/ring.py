@@ -57,6 +57,9 @@ class RingAttention:
             self.plans.append(FFAPlan([s[0:2] for s in sl], [s[2:4] for s in sl], [s[4] for s in sl], L,
                                       len(self.chunks_of[src]) * self.chunk_size, head_dim) if sl else None)
         self.comm_stream = torch.cuda.Stream(self.device)
+        # gloo point-to-point moves host memory only (the transport of ranks
+        # that share a GPU): K/V are then staged through the host
+        self.host_staged = dist.is_initialized() and dist.get_backend(group) != "nccl"
         self.L = _lib.lib()
 
     def local_token_index(self) -> torch.Tensor:
@@ -67,6 +70,18 @@ class RingAttention:
         """Send `tensors` to the next rank, receive same-shaped ones from the
         previous rank, on the comm stream. Returns (received, works)."""
         nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        if self.host_staged:
+            with torch.cuda.stream(self.comm_stream):
+                sends = [t.to("cpu") for t in tensors]
+            recv_h = [torch.empty_like(t) for t in sends]
+            ops = []
+            for t, r in zip(sends, recv_h):
+                ops.append(dist.P2POp(dist.isend, t, nxt, group=self.group))
+                ops.append(dist.P2POp(dist.irecv, r, prv, group=self.group))
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+            with torch.cuda.stream(self.comm_stream):
+                return [r.to(self.device) for r in recv_h], []
         with torch.cuda.stream(self.comm_stream):
             recv = [torch.empty_like(t) for t in tensors]
             ops = []

@@ -1,4 +1,4 @@
-"""Context-parallel FFA on 2 and 4 GPUs (NCCL), checked against the CPU
+"""Context-parallel FFA at 2 and 4 ranks, checked against the CPU
 oracle on the global sequence, and at the SURVEY §8d config-5 reduced shape
 (S = 65536, block-causal 8192, 48 q / 8 kv heads, greedy dispatch with the
 default chunk) against the dense fp32 reference on sampled rows.
@@ -7,6 +7,11 @@ The multi-stage schedule (§4.2 Alg. 2; reference sim.cpp:193-248) is
 forced with a cost model under which splitting is free and the cast is
 expensive, so the overlap solver takes `max_num_chunks` stages; every such
 case asserts that the executed plan really has more than one stage.
+
+One rank per GPU over NCCL when the box has enough GPUs; otherwise the ranks
+share the GPUs and talk over gloo (CUDA buffers staged through the host) —
+the same executor, kernels and stage schedule, only the transport differs
+(the C-ABI executor, NCCL-only, is skipped then).
 
 Tolerances (bf16 outputs from f32 accumulators; bf16 P / dS operands):
 O <= 1e-2 and dQ / dK / dV <= 1.5e-2 of max |ref|, LSE <= 2e-4 abs.
@@ -58,9 +63,13 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode, stages, check
     import torch.distributed as dist
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", rank % ndev)
+    torch.cuda.set_device(dev)
+    if ndev >= world:  # one rank per GPU: NCCL
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    else:  # ranks share GPUs (NCCL refuses that): gloo moves the CUDA buffers through the host
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_2505_13211_b200.cp import CPAttention
         from paper_2505_13211_b200.ring import RingAttention
@@ -176,8 +185,8 @@ CASES = [
 @pytest.mark.parametrize("mode,mask,chunk,stages", CASES,
                          ids=[f"{m}-{k['pattern']}-{k['seqlen']}-s{s}" for m, k, _, s in CASES])
 def test_cp_matches_oracle(built_lib, cuda, world, mode, mask, chunk, stages):
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
+    if torch.cuda.device_count() < world and mode == "capi":
+        pytest.skip(f"the C-ABI executor speaks NCCL, one rank per GPU: needs {world} GPUs")
     from oracle import oracle
     from paper_2505_13211_b200.planner import Mask
 
@@ -223,8 +232,6 @@ def test_cp_config5_reduced(built_lib, cuda, world, stages):
     48 q / 8 kv heads, greedy dispatch, default chunk S/cp/8): the bench's
     scenario (fitted B200 cost model) and a forced 3-package split; sampled
     rows and keys of every rank vs the dense fp32 reference."""
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs")
     chunk = 65536 // world // 8
     res = _launch(world, CFG5, chunk, 48, 8, 128, "magi", stages, "dense", next(_PORTS))
     for rank, nst, same, errs in res:
