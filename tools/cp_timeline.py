@@ -68,6 +68,8 @@ def main() -> None:
     ap.add_argument("--hq", type=int, default=48)
     ap.add_argument("--hk", type=int, default=8)
     ap.add_argument("--out", default="")
+    ap.add_argument("--bench", action="store_true",
+                    help="the bench's own scenario (cp_bench.scenario: fitted B200 cost model, solver's stages)")
     args = ap.parse_args()
 
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
@@ -82,6 +84,13 @@ def main() -> None:
                          "num_heads_q": args.hq, "num_heads_k": args.hk, "num_heads_v": args.hk, "head_dim": D},
             "cp_size": world, "cost_model": STAGED,
             "overlap": {"min_chunk_size": 512, "max_num_chunks": args.stages}}
+    if args.bench:
+        from paper_2505_13211_b200 import cp_bench
+
+        scen = cp_bench.scenario(world)
+        args.per_rank, args.block, args.hq, args.hk = cp_bench.PER_RANK, cp_bench.BLOCK, cp_bench.HQ, cp_bench.HK
+        S = args.per_rank * world
+        args.stages = None
     cpa = CPAttention(scen, args.hq, args.hk, D)
     L = cpa.local_tokens
     g = torch.Generator(device="cpu").manual_seed(rank)
