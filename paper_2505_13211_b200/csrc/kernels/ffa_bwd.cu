@@ -214,9 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   (void)tmap_do;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // head-major grid: co-running CTAs stream the same K / V (L2 resident).
-  // (The forward's GQA-group interleave measured 3% slower here on the
-  // varlen config and neutral on config 2.)
+  // head-major grid: co-running CTAs stream the same K / V (L2 resident)
   const int tile_rank = blockIdx.x % p.num_q_tiles;
   const int head = blockIdx.x / p.num_q_tiles;
   const int head_k = head / (p.hq / p.hk);

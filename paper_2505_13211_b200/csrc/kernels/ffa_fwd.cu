@@ -302,16 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
-  // grid order: one GQA group (the q heads of a kv head) at a time, its
-  // heads interleaved tile by tile in the plan's longest-first order, so
-  // co-running CTAs stream the same K / V (L2 resident) and the group's short
-  // tiles, not one head's long ones, form the tail (the makespan of a
-  // global longest-first list, without mixing K / V heads)
-  const int grp = p.hq / p.hk;
-  const int span = grp * p.num_tiles;
-  const int r_in = static_cast<int>(blockIdx.x) % span;
-  const int tile_rank = r_in / grp;
-  const int head = (static_cast<int>(blockIdx.x) / span) * grp + r_in % grp;
+  // head-major grid: co-running CTAs stream the same K / V (L2 resident)
+  const int tile_rank = blockIdx.x % p.num_tiles;
+  const int head = blockIdx.x / p.num_tiles;
   const int head_k = head / (p.hq / p.hk);
   const FwdTile tile = p.tiles[tile_rank];
   const int n_total = tile.n_ktiles;
