@@ -48,6 +48,38 @@ __global__ void range_gather_kernel(const uint4* __restrict__ src, uint4* __rest
   }
 }
 
+// Row-per-warp form for rows of >= 32 vectors (a K/V token row of 8 heads x
+// 128 x bf16 is 128): the range lookup is done once per row, and every lane
+// issues its kRowUnroll 16-byte loads before its stores, so each warp keeps
+// kRowUnroll x 512 B in flight instead of one dependent load per thread.
+constexpr int kRowUnroll = 4;
+__global__ void range_gather_rows_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                         const int64_t* __restrict__ ranges,
+                                         const int64_t* __restrict__ offsets, int64_t n,
+                                         int64_t total_rows, int64_t vec_per_row) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; r < total_rows;
+       r += warps) {
+    const int64_t j = find_range(offsets, n, r);
+    const uint4* s = src + (ranges[2 * j] + (r - offsets[j])) * vec_per_row;
+    uint4* d = dst + r * vec_per_row;
+    for (int64_t c0 = 0; c0 < vec_per_row; c0 += 32 * kRowUnroll) {
+      uint4 v[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) v[u] = s[c];
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) d[c] = v[u];
+      }
+    }
+  }
+}
+
 __global__ void range_scatter_add_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
                                          const int64_t* __restrict__ ranges,
                                          const int64_t* __restrict__ offsets, int64_t n,
@@ -68,6 +100,39 @@ __global__ void range_scatter_add_kernel(const float4* __restrict__ src, float4*
     a.z += b.z;
     a.w += b.w;
     dst[dst_row * vec_per_row + c] = a;
+  }
+}
+
+// Row-per-warp form of the scatter-add (rows of >= 32 vectors): one range
+// lookup per row, kRowUnroll source and destination vectors in flight per
+// lane. Same per-element order as above: one call's ranges never alias.
+__global__ void range_scatter_add_rows_kernel(const float4* __restrict__ src, float4* __restrict__ dst,
+                                              const int64_t* __restrict__ ranges,
+                                              const int64_t* __restrict__ offsets, int64_t n,
+                                              int64_t total_rows, int64_t vec_per_row) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; r < total_rows;
+       r += warps) {
+    const int64_t j = find_range(offsets, n, r);
+    float4* d = dst + (ranges[2 * j] + (r - offsets[j])) * vec_per_row;
+    const float4* s = src + r * vec_per_row;
+    for (int64_t c0 = 0; c0 < vec_per_row; c0 += 32 * kRowUnroll) {
+      float4 a[kRowUnroll], b[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) {
+          a[u] = d[c];
+          b[u] = s[c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) d[c] = make_float4(a[u].x + b[u].x, a[u].y + b[u].y, a[u].z + b[u].z, a[u].w + b[u].w);
+      }
+    }
   }
 }
 
@@ -167,9 +232,15 @@ cudaError_t launch_range_gather(const void* src, void* dst, const int64_t* range
                                 int64_t row_bytes, cudaStream_t stream) {
   if (num_ranges == 0 || total_rows == 0) return cudaSuccess;
   const int64_t vec = row_bytes / 16;
-  range_gather_kernel<<<grid_for(total_rows * vec, 256), 256, 0, stream>>>(
-      static_cast<const uint4*>(src), static_cast<uint4*>(dst), ranges, offsets, num_ranges,
-      total_rows, vec);
+  if (vec >= 32) {
+    range_gather_rows_kernel<<<grid_for(total_rows * 32, 256), 256, 0, stream>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), ranges, offsets, num_ranges,
+        total_rows, vec);
+  } else {
+    range_gather_kernel<<<grid_for(total_rows * vec, 256), 256, 0, stream>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), ranges, offsets, num_ranges,
+        total_rows, vec);
+  }
   return cudaGetLastError();
 }
 
@@ -179,9 +250,15 @@ cudaError_t launch_range_scatter_add_f32(const float* src, float* dst, const int
                                          cudaStream_t stream) {
   if (num_ranges == 0 || total_rows == 0) return cudaSuccess;
   const int64_t vec = row_elems / 4;
-  range_scatter_add_kernel<<<grid_for(total_rows * vec, 256), 256, 0, stream>>>(
-      reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), ranges, offsets,
-      num_ranges, total_rows, vec);
+  if (vec >= 32) {
+    range_scatter_add_rows_kernel<<<grid_for(total_rows * 32, 256), 256, 0, stream>>>(
+        reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), ranges, offsets,
+        num_ranges, total_rows, vec);
+  } else {
+    range_scatter_add_kernel<<<grid_for(total_rows * vec, 256), 256, 0, stream>>>(
+        reinterpret_cast<const float4*>(src), reinterpret_cast<float4*>(dst), ranges, offsets,
+        num_ranges, total_rows, vec);
+  }
   return cudaGetLastError();
 }
 
