@@ -103,18 +103,23 @@ def test_stage_backward_and_prepare(built_lib, cuda):
     plan.prepare()
     out, lse = ffa_forward(plan, q, k, v, out_dtype=torch.float32)
     dq0, dk0, dv0 = ffa_backward(plan, q, k, v, out, lse, do, grad_dtype=torch.float32)
-    delta = (do.float() * out).sum(-1).t().contiguous()
-    run = torch.randn(sq, hq, d, device=cuda)  # running dQ of earlier stages
+    L = _lib.lib()
+    # delta by the library's own preprocess, as ffa_backward computes it (a
+    # torch row sum rounds differently and dS = P (dP - delta) amplifies it)
+    delta = torch.empty(hq, sq, device=cuda)
+    _lib.check(L.magiplan_ffa_bwd_preprocess(out.data_ptr(), do.data_ptr(), delta.data_ptr(), sq, hq, d, _lib.F32,
+                                             torch.cuda.current_stream().cuda_stream))
+    g = torch.Generator(device="cpu").manual_seed(81)
+    run = torch.randn(sq, hq, d, generator=g).to(cuda)  # running dQ of earlier stages
     dq = run.clone()
     dk = torch.full((sk, hk, d), 7.0, device=cuda)  # garbage: must be overwritten
     dv = torch.full_like(dk, -3.0)
-    L = _lib.lib()
     _lib.check(L.magiplan_ffa_bwd_stage(plan.handle, q.data_ptr(), k.data_ptr(), v.data_ptr(), lse.data_ptr(),
                                         delta.data_ptr(), do.data_ptr(), dq.data_ptr(), dk.data_ptr(),
                                         dv.data_ptr(), hq, hk, 1.0 / math.sqrt(d),
                                         torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
-    assert torch.allclose(dq, run + dq0, rtol=1e-5, atol=1e-5)
+    assert torch.allclose(dq, run + dq0, rtol=1e-6, atol=1e-6), (dq - run - dq0).abs().max()
     assert torch.equal(dk, dk0) and torch.equal(dv, dv0)
 
 
