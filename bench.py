@@ -254,6 +254,13 @@ def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # all the host's threads for the CPU path: torchrun exports
+    # OMP_NUM_THREADS=1 to every rank, and the oracle shares torch's OpenMP
+    # runtime, so reset both before the first parallel region
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
+    import torch
+
+    torch.set_num_threads(os.cpu_count() or 1)
     wl = WORKLOADS[args.workload]
     world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
     if world > 1:
