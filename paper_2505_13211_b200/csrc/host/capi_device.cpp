@@ -11,7 +11,7 @@
 namespace magi {
 cudaError_t launch_umma_tile(const void* a, const void* b, float* c, int b_mn_major,
                              cudaStream_t stream);
-cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_tiles,
+cudaError_t launch_ffa_fwd(const FwdWork& work,
                            int seqlen_q, int seqlen_k, int hq, int hk, int head_dim,
                            float softmax_scale, const void* q, const void* k, const void* v,
                            void* out, float* lse, int out_f32, int accumulate,
@@ -151,8 +151,7 @@ magiplan_status magiplan_ffa_fwd(const magiplan_ffa_plan* plan, const void* q, c
     check_dtype(out_dtype, accumulate);
     auto& P = const_cast<magiplan_ffa_plan*>(plan)->plan;
     magiplan::ensure_uploaded(P);
-    cuda_check(magi::launch_ffa_fwd(P.d_fwd2_tiles, P.d_fwd2_items,
-                                    static_cast<int>(P.fwd2_tiles.size()),
+    cuda_check(magi::launch_ffa_fwd(magiplan::fwd_work(P),
                                     static_cast<int>(P.seqlen_q), static_cast<int>(P.seqlen_k),
                                     static_cast<int>(num_heads_q), static_cast<int>(num_heads_k),
                                     P.head_dim, softmax_scale, q, k, v, out, lse,

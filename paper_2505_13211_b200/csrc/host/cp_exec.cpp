@@ -33,7 +33,7 @@
 #include "scenario.hpp"
 
 namespace magi {
-cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_tiles, int seqlen_q, int seqlen_k,
+cudaError_t launch_ffa_fwd(const FwdWork& work, int seqlen_q, int seqlen_k,
                            int hq, int hk, int head_dim, float softmax_scale, const void* q, const void* k,
                            const void* v, void* out, float* lse, int out_f32, int accumulate, cudaStream_t stream);
 cudaError_t launch_ffa_bwd_preprocess(const void* out, const void* grad_out, float* delta, int64_t seqlen,
@@ -420,7 +420,7 @@ magiplan_status magiplan_cp_forward(magiplan_cp* cp, const void* q, const void* 
     if (!ex.fwd.empty()) casts.push_back(ex.cast(ex.fwd[0], k, v));
     auto ffa = [&](const magiplan_ffa_plan* pl, const void* kk, const void* vv, int acc) {
       const FfaPlan& P = pl->plan;
-      cuda_check(magi::launch_ffa_fwd(P.d_fwd2_tiles, P.d_fwd2_items, static_cast<int>(P.fwd2_tiles.size()),
+      cuda_check(magi::launch_ffa_fwd(magiplan::fwd_work(P),
                                       static_cast<int>(P.seqlen_q), static_cast<int>(P.seqlen_k), hq, hk, ex.d,
                                       ex.scale, q, kk, vv, out_f32, lse, 1, acc, cur),
                  "ffa_fwd launch");

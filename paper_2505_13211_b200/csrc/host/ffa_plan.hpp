@@ -54,4 +54,10 @@ void build_ffa_worklists(FfaPlan& plan);
 // plan is later used from a different device than the one it lives on.
 void ensure_uploaded(FfaPlan& plan);
 
+// Device work lists of an uploaded plan, both q-tile heights.
+inline magi::FwdWork fwd_work(const FfaPlan& P) {
+  return {P.d_fwd_tiles, P.d_fwd_items, static_cast<int32_t>(P.fwd_tiles.size()),
+          P.d_fwd2_tiles, P.d_fwd2_items, static_cast<int32_t>(P.fwd2_tiles.size())};
+}
+
 }  // namespace magiplan

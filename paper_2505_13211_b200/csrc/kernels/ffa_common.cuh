@@ -50,6 +50,18 @@ struct FwdTile {
   int32_t n_ktiles;    // total key tiles over the items (LPT weight)
 };
 
+// A forward work list at both q-tile heights the planner builds (128 rows:
+// FfaPlan::fwd_*, 256 rows: fwd2_*); the launcher uses the one its kernel
+// layout tiles by.
+struct FwdWork {
+  const FwdTile* tiles128;
+  const FwdItem* items128;
+  int32_t num_tiles128;
+  const FwdTile* tiles256;
+  const FwdItem* items256;
+  int32_t num_tiles256;
+};
+
 // One (key tile, slice) intersection for the k-major backward kernel: query
 // tiles [q_begin + i*128, ...) for i < n_qtiles.
 struct BwdItem {

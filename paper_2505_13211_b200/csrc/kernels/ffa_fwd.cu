@@ -491,17 +491,17 @@ cudaError_t launch_fwd_impl(const FwdParams& prm, const void* q, const void* k, 
 
 }  // namespace
 
-// tiles/items: the plan's 256-row q-major work list (FfaPlan::fwd2_*).
-cudaError_t launch_ffa_fwd(const FwdTile* tiles, const FwdItem* items, int num_tiles,
+// work: the plan's q-major work lists; this layout tiles by 256 rows (fwd2_*).
+cudaError_t launch_ffa_fwd(const FwdWork& work,
                            int seqlen_q, int seqlen_k, int hq, int hk, int head_dim,
                            float softmax_scale, const void* q, const void* k, const void* v,
                            void* out, float* lse, int out_f32, int accumulate,
                            cudaStream_t stream) {
-  if (num_tiles == 0 || hq == 0) return cudaSuccess;
+  if (work.num_tiles256 == 0 || hq == 0) return cudaSuccess;
   FwdParams prm;
-  prm.tiles = tiles;
-  prm.items = items;
-  prm.num_tiles = num_tiles;
+  prm.tiles = work.tiles256;
+  prm.items = work.items256;
+  prm.num_tiles = work.num_tiles256;
   prm.seqlen_q = seqlen_q;
   prm.seqlen_k = seqlen_k;
   prm.hq = hq;
