@@ -22,6 +22,23 @@ def varlen(lengths, types):
     return qr, kr, list(types)
 
 
+def random_slices(sq, sk, n, seed):
+    """n random (possibly overlapping, possibly non-square) slices of all four
+    types: MULTIPLICITY semantics and the diagonal anchors of every type on
+    tiles that start and end mid-tile."""
+    rng = np.random.default_rng(seed)
+    qr, kr, ty = [], [], []
+    while len(qr) < n:
+        a, b = sorted(int(x) for x in rng.integers(0, sq + 1, 2))
+        c, e = sorted(int(x) for x in rng.integers(0, sk + 1, 2))
+        if b - a < 1 or e - c < 1:
+            continue
+        qr.append([a, b])
+        kr.append([c, e])
+        ty.append(int(rng.integers(0, 4)))
+    return qr, kr, ty
+
+
 # name -> (sq, sk, hq, hk, d, q_ranges, k_ranges, types)
 CASES = {
     "cfg1_block_causal_d64": (1024, 1024, 1, 1, 64, *block_causal(1024, 256)),
@@ -53,6 +70,10 @@ CASES = {
                        *varlen([1 + (7 * i) % 31 for i in range(41)], [i % 2 for i in range(41)])),
     # GQA 6:1 at head_dim 64, unaligned causal
     "gqa6_causal_d64": (333, 333, 6, 1, 64, [[0, 333]], [[0, 333]], [CAUSAL]),
+    # GQA 16:1 (a single kv head): the dK/dV pass walks 16 q heads per key tile
+    "gqa16_block_causal": (512, 512, 16, 1, 128, *block_causal(512, 128)),
+    # 12 random overlapping slices of all four types, sq != sk
+    "random_overlapping": (700, 900, 2, 1, 128, *random_slices(700, 900, 12, seed=2025)),
 }
 
 
