@@ -21,7 +21,9 @@
  * Mask semantics are pinned against the compiled reference (tests/golden);
  * the numerics themselves are "parity unpinned" by the reference (it has no
  * golden numerics) and are cross-checked against an independent dense torch
- * float64 formulation in tests/test_oracle.py.
+ * float64 formulation and against PyTorch's own scaled_dot_product_attention
+ * (float64, autograd; every non-overlapping case, 1e-9) in
+ * tests/test_oracle.py.
  *
  * Accumulation is double (acc_f32 == 0) or float (acc_f32 == 1; the CPU
  * baseline timed by bench.py). Inputs are float arrays holding the

@@ -127,3 +127,50 @@ def test_dense_fp32_reference_matches_oracle(name):
     for got, ref in ((out.numpy(), ro), (dq.numpy(), rdq[rows]), (dk.numpy(), rdk[keys]),
                      (dv.numpy(), rdv[keys])):
         assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("name", ["cfg1_block_causal_d64", "block_causal_gqa_d128", "causal_unaligned",
+                                  "varlen_mixed", "inv_bi_d64", "empty_rows", "cross_lk_gt_lq",
+                                  "causal_lq_gt_lk", "sliding_window", "uncovered_keys", "many_tiny_docs",
+                                  "gqa6_causal_d64", "gqa16_block_causal"])
+def test_oracle_matches_torch_sdpa(name):
+    """A third, external pin of the oracle's numerics: PyTorch's own
+    scaled_dot_product_attention (float64, math kernel, autograd) with the
+    boolean mask of the slice list (membership from the reference-pinned
+    oracle.dense_allowed), on every case whose slices do not overlap (SDPA
+    has no multiplicity). Rows without keys are left out (SDPA returns NaN
+    there; their dO is zeroed so they add nothing to dK / dV)."""
+    import torch.nn.functional as F
+
+    from tests.ffa_cases import CASES, make_inputs
+
+    sq, sk, hq, hk, d, qr, kr, ty = CASES[name]
+    cnt = oracle.dense_allowed(sq, sk, qr, kr, ty)
+    assert cnt.max() <= 1, "overlapping slices: not expressible as an SDPA mask"
+    q, k, v, do = make_inputs(sq, sk, hq, hk, d, seed=4, device="cpu")
+    scale = 1.0 / math.sqrt(d)
+    ro, rl = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale)
+    rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ro, rl, do, qr, kr, ty, scale)
+
+    has = cnt.sum(axis=1) > 0
+    mask = torch.from_numpy(cnt > 0)
+    mask[~torch.from_numpy(has)] = True  # keep SDPA finite on empty rows (excluded below)
+    g = hq // hk
+    qd = q.double().permute(1, 0, 2).requires_grad_(True)            # [hq, sq, d]
+    kd = k.double().permute(1, 0, 2).requires_grad_(True)            # [hk, sk, d]
+    vd = v.double().permute(1, 0, 2).requires_grad_(True)
+    o = F.scaled_dot_product_attention(qd, kd.repeat_interleave(g, 0), vd.repeat_interleave(g, 0),
+                                       attn_mask=mask, scale=scale)
+    dod = do.double().permute(1, 0, 2) * torch.from_numpy(has)[None, :, None]
+    o.backward(dod)
+    o = o.detach().permute(1, 0, 2).numpy()
+    sdq = qd.grad.permute(1, 0, 2).numpy()
+    sdk = kd.grad.permute(1, 0, 2).numpy()
+    sdv = vd.grad.permute(1, 0, 2).numpy()
+    tol = 1e-9 * max(1.0, float(np.abs(ro).max()))
+    assert np.abs(o[has] - ro[has]).max() <= tol
+    assert np.all(ro[~has] == 0) and np.all(np.isneginf(rl[:, ~has]))
+    assert np.abs(sdq[has] - rdq[has]).max() <= 1e-9 * max(1.0, float(np.abs(rdq).max()))
+    assert np.abs(sdk - rdk).max() <= 1e-9 * max(1.0, float(np.abs(rdk).max()))
+    assert np.abs(sdv - rdv).max() <= 1e-9 * max(1.0, float(np.abs(rdv).max()))
+
