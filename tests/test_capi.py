@@ -156,3 +156,109 @@ def test_ffa_plan_validation_on_cpu(built_lib):
     assert st == _lib.ERR_USAGE and b"exceeds mask bounds" in L.magiplan_last_error()
     st = L.magiplan_ffa_plan_create(qr, kr, ty, 1, 300, 300, 96, C.byref(h))
     assert st == _lib.ERR_USAGE and b"head_dim" in L.magiplan_last_error()
+
+
+# ---------------------------------------------------------------- a plain C consumer
+def _build_c_consumer() -> Path:
+    """gcc-compile tests/c_consumer/ffa_consumer.c against include/ and the
+    in-tree libmagiplan.so (+ the CUDA runtime for its device buffers): the
+    link a C client of the reference planner does after the switch."""
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    cuda = Path("/usr/local/cuda")
+    out = ROOT / "build" / "c_consumer" / "ffa_consumer"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    pkg = ROOT / "paper_2505_13211_b200"
+    cmd = ["gcc", "-O2", "-std=c11", str(ROOT / "tests" / "c_consumer" / "ffa_consumer.c"),
+           f"-I{ROOT / 'include'}", f"-I{cuda / 'include'}", f"-L{pkg}", "-lmagiplan",
+           f"-L{cuda / 'lib64'}", "-lcudart", "-lm", f"-Wl,-rpath,{pkg}", f"-Wl,-rpath,{cuda / 'lib64'}",
+           "-o", str(out)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    assert res.returncode == 0, res.stderr
+    return out
+
+
+def test_c_consumer_planner(built_lib):
+    """The reference's own entry points called from C (no Python in the
+    process): the mask area and the scenario plan match the ctypes path."""
+    import subprocess
+
+    from paper_2505_13211_b200 import _lib
+    from paper_2505_13211_b200.planner import Mask, Scenario
+
+    exe = _build_c_consumer()
+    res = subprocess.run([str(exe), "plan"], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stderr
+    area, nbytes = (int(x) for x in res.stdout.split()[1::2])
+    assert area == Mask({"seqlen": 32768, "pattern": "block_causal", "params": {"block_size": 4096}}).area()
+    scen = {"workload": {"mask": {"seqlen": 131072, "pattern": "block_causal", "params": {"block_size": 8192}},
+                         "num_heads_q": 48, "num_heads_k": 8, "num_heads_v": 8, "head_dim": 128},
+            "cp_size": 4}
+    assert nbytes == len(Scenario(scen).plan_text().encode())
+    assert _lib is not None
+
+
+def _xorshift_bf16(n: int, state: list[int]):
+    """The consumer's input stream (xorshift32 -> uniform [-1, 1) -> bf16,
+    round to nearest even), regenerated bit for bit."""
+    import numpy as np
+
+    out = np.empty(n, np.float32)
+    s = state[0]
+    for i in range(n):
+        s ^= (s << 13) & 0xFFFFFFFF
+        s ^= s >> 17
+        s ^= (s << 5) & 0xFFFFFFFF
+        out[i] = np.float32((s >> 8) / 16777216.0 * 2.0 - 1.0)
+    state[0] = s
+    u = out.view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
+    return (u.astype(np.uint32) << 16).view(np.float32)
+
+
+@pytest.mark.gpu
+def test_c_consumer_ffa_matches_oracle(built_lib, cuda, tmp_path):
+    """FFA forward + backward driven from C through the ABI (cudaMalloc'd
+    buffers, a cudaStream_t, no torch in the process), checked against the
+    CPU oracle on the same inputs: 640 tokens, block-causal 128 plus an
+    overlapping causal slice, 4 q / 2 kv heads, d = 128, f32 outputs."""
+    import math
+    import subprocess
+
+    import numpy as np
+    from oracle import oracle
+
+    exe = _build_c_consumer()
+    path = tmp_path / "ffa.bin"
+    res = subprocess.run([str(exe), "ffa", str(path)], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stderr
+    S, HQ, HK, D = 640, 4, 2, 128
+    qr = [[0, 128], [128, 256], [256, 384], [384, 512], [512, 640], [0, 200]]
+    kr = [[0, 128], [0, 256], [0, 384], [0, 512], [0, 640], [0, 200]]
+    ty = [0, 0, 0, 0, 0, 1]
+    st = [12345]
+    q = _xorshift_bf16(S * HQ * D, st).reshape(S, HQ, D)
+    k = _xorshift_bf16(S * HK * D, st).reshape(S, HK, D)
+    v = _xorshift_bf16(S * HK * D, st).reshape(S, HK, D)
+    do = _xorshift_bf16(S * HQ * D, st).reshape(S, HQ, D)
+    raw = np.fromfile(path, np.float32)
+    sizes = [S * HQ * D, HQ * S, S * HQ * D, S * HK * D, S * HK * D]
+    parts, off = [], 0
+    for n in sizes:
+        parts.append(raw[off:off + n])
+        off += n
+    o, lse, dq, dk, dv = parts
+    scale = 1.0 / math.sqrt(D)
+    ro, rl = oracle.ffa_fwd(q, k, v, qr, kr, ty, scale)
+    rdq, rdk, rdv = oracle.ffa_bwd(q, k, v, ro, rl, do, qr, kr, ty, scale)
+
+    def rel(a, b):
+        return float(np.abs(a - b).max() / np.abs(b).max())
+
+    assert rel(o.reshape(ro.shape), ro) < 5e-3
+    assert float(np.abs(lse.reshape(rl.shape) - rl).max()) < 2e-4
+    for got, ref in ((dq, rdq), (dk, rdk), (dv, rdv)):
+        assert rel(got.reshape(ref.shape), ref) < 1e-2
