@@ -213,6 +213,31 @@ MAGIPLAN_API magiplan_status magiplan_range_scatter_add_f32(const float* src, fl
 MAGIPLAN_API magiplan_status magiplan_cast_f32_bf16(const float* src, void* dst, int64_t n,
                                                     void* cuda_stream);
 
+/* ---- peer-memory exchange (new): the GroupCast without NCCL -------------
+ * Device buffers another process on the node can map (CUDA IPC): malloc
+ * returns the pointer and its 64-byte handle; open maps a peer's handle. */
+MAGIPLAN_API magiplan_status magiplan_p2p_malloc(int64_t bytes, void** out_ptr,
+                                                 unsigned char* out_handle);
+MAGIPLAN_API magiplan_status magiplan_p2p_free(void* ptr);
+MAGIPLAN_API magiplan_status magiplan_p2p_open(const unsigned char* handle, void** out_ptr);
+MAGIPLAN_API magiplan_status magiplan_p2p_close(void* ptr);
+/* Range Gather fused with the transfer: range i copies source rows
+ * [ranges[2i], ranges[2i+1]) to rows dst_row[i].. of the buffer at
+ * dst_base[i] (device arrays; bases may be peer-mapped). offsets: packed
+ * prefix of the range lengths, total_rows their sum. */
+MAGIPLAN_API magiplan_status magiplan_range_copy_to(const void* src, const int64_t* ranges,
+                                                    const int64_t* offsets, const uint64_t* dst_base,
+                                                    const int64_t* dst_row, int64_t num_ranges,
+                                                    int64_t total_rows, int64_t row_bytes,
+                                                    void* cuda_stream);
+/* Stream-ordered flags: a system-scope release store of `value` to each of
+ * the n <= 32 flags whose addresses are in the device array flag_ptrs; and a
+ * wait until flags[i] >= value for every set bit i of mask (acquire). */
+MAGIPLAN_API magiplan_status magiplan_flags_signal(const uint64_t* flag_ptrs, int32_t n, uint32_t value,
+                                                   void* cuda_stream);
+MAGIPLAN_API magiplan_status magiplan_flags_wait(const uint32_t* flags, uint32_t mask, uint32_t value,
+                                                 void* cuda_stream);
+
 /* ---- context-parallel executor (new) ------------------------------------ */
 /* The planner's multi-stage CP schedule run on this process's GPU (one
  * process per GPU): GroupCast / GroupReduce over NCCL point-to-point

@@ -56,6 +56,13 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_range_gather": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "magiplan_range_scatter_add_f32": (C.c_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "magiplan_cast_f32_bf16": (C.c_int, [_vp, _vp, _i64, _vp]),
+    "magiplan_p2p_malloc": (C.c_int, [_i64, C.POINTER(C.c_void_p), C.c_char_p]),
+    "magiplan_p2p_free": (C.c_int, [_vp]),
+    "magiplan_p2p_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
+    "magiplan_p2p_close": (C.c_int, [_vp]),
+    "magiplan_range_copy_to": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "magiplan_flags_signal": (C.c_int, [_vp, _i32, C.c_uint32, _vp]),
+    "magiplan_flags_wait": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _vp]),
     "magiplan_debug_umma_tile": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),
     "magiplan_debug_eval": (C.c_int, [_cp, C.POINTER(_vp)]),
     "magiplan_debug_set_trace": (C.c_int, [_vp, _i32]),

@@ -102,7 +102,14 @@ class CPAttention:
     """
 
     def __init__(self, scenario: dict | str, num_heads_q: int, num_heads_k: int, head_dim: int,
-                 group=None, device=None, softmax_scale: float | None = None):
+                 group=None, device=None, softmax_scale: float | None = None, transport: str = "nccl"):
+        """transport: "nccl" (GroupCast / GroupReduce as NCCL all-to-alls) or
+        "p2p" (the forward GroupCast as one range-copy kernel writing straight
+        into the consumers' receive buffers over NVLink, mapped with CUDA IPC,
+        ordered by stream-side flags; one rank per GPU, GroupReduce on NCCL)."""
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport {transport!r}: 'nccl' or 'p2p'")
+        self.transport = transport
         self.group = group
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -156,6 +163,129 @@ class CPAttention:
             self.reduce_group = _new_group(ranks)
         self.L = _lib.lib()
         self.timeline: list | None = None  # set to [] to record per-stage CUDA events
+        self._p2p: list[dict] = []
+        self._p2p_epoch = 0
+        self._p2p_owned: list[int] = []
+        self._p2p_opened: list[int] = []
+        if transport == "p2p" and self.world > 1:
+            self._setup_p2p()
+
+    # ------------------------------------------------------------ peer memory
+    def _setup_p2p(self):
+        """Per forward stage: receive buffers and a flag block [ready[cp] |
+        consumed[cp]] in IPC-exportable memory, handles exchanged once, the
+        peers' buffers mapped, and the device arrays of the fused
+        gather-and-send kernel built from the executor plan (every
+        consumer's receive entries from this rank, at their buffer rows)."""
+        import ctypes as C
+
+        cp, me, L = self.world, self.rank, self.L
+        if cp > 32:
+            raise ValueError("p2p transport: at most 32 ranks (flag masks)")
+        row = self.hk * self.d * 2
+
+        def alloc(nbytes):
+            ptr, h = C.c_void_p(), C.create_string_buffer(64)
+            _lib.check(L.magiplan_p2p_malloc(nbytes, C.byref(ptr), h))
+            self._p2p_owned.append(ptr.value)
+            return ptr.value, h.raw
+
+        def view(ptr, n, dtype):
+            class _Raw:
+                __cuda_array_interface__ = {"shape": (n,), "typestr": "<i2" if dtype == torch.bfloat16 else "<i4",
+                                            "data": (ptr, False), "version": 3, "strides": None}
+            t = torch.as_tensor(_Raw(), device=self.device)
+            return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+
+        local, handles = [], []
+        for st in self.fwd_stages:
+            n = max(st.buf_tokens, 1) * self.hk * self.d
+            kp, kh = alloc(n * 2)
+            vp, vh = alloc(n * 2)
+            fp, fh = alloc(2 * cp * 4)
+            view(fp, 2 * cp, torch.int32).zero_()
+            local.append((kp, vp, fp))
+            handles.append((kh, vh, fh))
+        torch.cuda.synchronize(self.device)
+        every = [None] * cp
+        dist.all_gather_object(every, handles, group=self.group)
+        ranks = self.xplan["ranks"]
+
+        def dev64(vals, dtype=torch.int64):
+            return torch.tensor(vals if vals else [0], dtype=dtype, device=self.device)
+
+        for j, st in enumerate(self.fwd_stages):
+            kp, vp, fp = local[j]
+            peer = {}
+            for d in range(cp):
+                if d == me:
+                    continue
+                ptrs = []
+                for h in every[d][j]:
+                    out = C.c_void_p()
+                    _lib.check(L.magiplan_p2p_open(h, C.byref(out)))
+                    self._p2p_opened.append(out.value)
+                    ptrs.append(out.value)
+                peer[d] = ptrs
+            ranges, offs, kbase, vbase, drow, sig_send, wait_send = [], [], [], [], [], [], 0
+            acc = 0
+            for d in range(cp):
+                if d == me or j >= len(ranks[d]["fwd_stages"]):
+                    continue
+                mine = [e for e in ranks[d]["fwd_stages"][j]["recv"] if e[0] == me]
+                for _src, gs, ge, src_local, buf_off in mine:
+                    ranges += [src_local, src_local + (ge - gs)]
+                    offs.append(acc)
+                    acc += ge - gs
+                    kbase.append(peer[d][0])
+                    vbase.append(peer[d][1])
+                    drow.append(buf_off)
+                if mine:
+                    sig_send.append(peer[d][2] + 4 * me)      # d's ready[me]
+                    wait_send |= 1 << d                        # my consumed[d]
+            srcs = sorted({e[0] for e in ranks[me]["fwd_stages"][j]["recv"]})
+            self._p2p.append({
+                "kb": view(kp, max(st.buf_tokens, 1) * self.hk * self.d, torch.bfloat16)
+                .view(-1, self.hk, self.d)[:st.buf_tokens],
+                "vb": view(vp, max(st.buf_tokens, 1) * self.hk * self.d, torch.bfloat16)
+                .view(-1, self.hk, self.d)[:st.buf_tokens],
+                "flags": fp, "rows": acc, "n": len(offs), "row_bytes": row,
+                "ranges": dev64(ranges), "offs": dev64(offs), "drow": dev64(drow),
+                "kbase": dev64(kbase), "vbase": dev64(vbase),
+                "sig_send": dev64(sig_send), "n_sig_send": len(sig_send), "wait_send": wait_send,
+                "wait_recv": sum(1 << s_ for s_ in srcs),
+                "sig_recv": dev64([peer[s_][2] + 4 * (cp + me) for s_ in srcs]),
+                "n_sig_recv": len(srcs),
+            })
+
+    def close(self):
+        """Release the peer-memory mappings and buffers (p2p transport)."""
+        if not self._p2p_owned and not self._p2p_opened:
+            return
+        torch.cuda.synchronize(self.device)
+        for ptr in self._p2p_opened:
+            self.L.magiplan_p2p_close(ptr)
+        for ptr in self._p2p_owned:
+            self.L.magiplan_p2p_free(ptr)
+        self._p2p_opened, self._p2p_owned, self._p2p = [], [], []
+
+    def _cast_p2p(self, j: int, k: torch.Tensor, v: torch.Tensor):
+        """Forward GroupCast of stage j over peer memory, on the comm stream:
+        wait until every consumer has released this stage's buffer from the
+        previous pass, copy the ranges into the consumers' buffers, then
+        raise their ready flags. Same return shape as _cast."""
+        P, L, e = self._p2p[j], self.L, self._p2p_epoch
+        sp = self.comm_stream.cuda_stream
+        with torch.cuda.stream(self.comm_stream):
+            e0 = self._ev(self.comm_stream)
+            _lib.check(L.magiplan_flags_wait(P["flags"] + 4 * self.world, P["wait_send"], e - 1, sp))
+            if P["n"]:
+                for src, base in ((k, P["kbase"]), (v, P["vbase"])):
+                    _lib.check(L.magiplan_range_copy_to(src.data_ptr(), P["ranges"].data_ptr(),
+                                                        P["offs"].data_ptr(), base.data_ptr(), P["drow"].data_ptr(),
+                                                        P["n"], P["rows"], P["row_bytes"], sp))
+            _lib.check(L.magiplan_flags_signal(P["sig_send"].data_ptr(), P["n_sig_send"], e, sp))
+        return P["kb"], P["vb"], [], None, e0
 
     # ------------------------------------------------------------ tracing
     def _ev(self, stream):
@@ -272,8 +402,12 @@ class CPAttention:
         cur = torch.cuda.current_stream(q.device)
         self.comm_stream.wait_stream(cur)
         keep = []  # receive and send buffers of every stage, until the pass ends
+        p2p = bool(self._p2p)
+        if p2p:
+            self._p2p_epoch += 1
+        cast = (lambda j: self._cast_p2p(j, k, v)) if p2p else (lambda j: self._cast(self.fwd_stages[j], k, v))
         # step 0: cast(1) is issued first, then the host-local FFA
-        pending = self._cast(self.fwd_stages[0], k, v) if self.fwd_stages else None
+        pending = cast(0) if self.fwd_stages else None
         e0 = self._ev(cur)
         if self.host_plan is not None:
             ffa_forward(self.host_plan, q, k, v, self.scale, out=out, lse=lse)
@@ -283,15 +417,27 @@ class CPAttention:
         self._span("fwd", "ffa", 0, e0, self._ev(cur))
         for j, st in enumerate(self.fwd_stages):
             kb, vb, works, sent, ec = pending
-            keep.append((kb, vb, sent))
+            if not p2p:
+                keep.append((kb, vb, sent))
             # step j+1: cast(j+2) || ffa(j+1)
             if j + 1 < len(self.fwd_stages):
-                pending = self._cast(self.fwd_stages[j + 1], k, v)
-            self._cast_done("fwd", j + 1, works, ec)
+                pending = cast(j + 1)
+            if p2p:
+                # the peers' copies into this rank's buffer have landed
+                P = self._p2p[j]
+                _lib.check(self.L.magiplan_flags_wait(P["flags"], P["wait_recv"], self._p2p_epoch, cur.cuda_stream))
+                if self.timeline is not None:
+                    self._span("fwd", "cast", j + 1, ec, self._ev(cur))
+            else:
+                self._cast_done("fwd", j + 1, works, ec)
             e0 = self._ev(cur)
             if st.plan is not None:
                 ffa_forward(st.plan, q, kb, vb, self.scale, out=out, lse=lse, accumulate=True)
             self._span("fwd", "ffa", j + 1, e0, self._ev(cur))
+            if p2p:
+                # release the buffer: the producers may overwrite it next pass
+                _lib.check(self.L.magiplan_flags_signal(P["sig_recv"].data_ptr(), P["n_sig_recv"],
+                                                        self._p2p_epoch, cur.cuda_stream))
         out_bf = torch.empty((L, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
         _lib.check(self.L.magiplan_cast_f32_bf16(out.data_ptr(), out_bf.data_ptr(), out.numel(),
                                                  cur.cuda_stream))

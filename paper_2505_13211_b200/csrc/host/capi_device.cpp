@@ -4,6 +4,8 @@
 // caller's stream and maps CUDA launch failures to MAGIPLAN_ERR_INTERNAL.
 #include <cuda_runtime.h>
 
+#include <cstring>
+
 #include "capi_util.hpp"
 #include "ffa_plan.hpp"
 #include "mask.hpp"
@@ -26,6 +28,12 @@ cudaError_t launch_ffa_bwd(const FwdTile* q_tiles, const FwdItem* q_items, int n
                            const float* lse, const float* delta, const void* grad_out,
                            void* grad_q, void* grad_k, void* grad_v, int grad_f32,
                            int accumulate, int parts, cudaStream_t stream);
+cudaError_t launch_range_copy_to(const void* src, const int64_t* ranges, const int64_t* offsets,
+                                 const unsigned long long* dst_base, const int64_t* dst_row, int64_t num_ranges,
+                                 int64_t total_rows, int64_t row_bytes, cudaStream_t stream);
+cudaError_t launch_flags_signal(unsigned int* const* flags, int n, unsigned int value, cudaStream_t stream);
+cudaError_t launch_flags_wait(const unsigned int* flags, unsigned int mask, unsigned int value,
+                              cudaStream_t stream);
 cudaError_t launch_range_gather(const void* src, void* dst, const int64_t* ranges,
                                 const int64_t* offsets, int64_t num_ranges, int64_t total_rows,
                                 int64_t row_bytes, cudaStream_t stream);
@@ -273,6 +281,71 @@ magiplan_status magiplan_range_scatter_add_f32(const float* src, float* dst,
     cuda_check(magi::launch_range_scatter_add_f32(src, dst, ranges, offsets, num_ranges,
                                                   total_rows, row_elems, as_stream(cuda_stream)),
                "range_scatter_add launch");
+  });
+}
+
+// ---------------------------------------------------------------- peer memory
+magiplan_status magiplan_p2p_malloc(int64_t bytes, void** out_ptr, unsigned char* out_handle) {
+  MAGI_REQUIRE(out_ptr && out_handle);
+  return guarded([&] {
+    if (bytes <= 0) throw UsageError("p2p_malloc: bytes must be > 0");
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, static_cast<size_t>(bytes)), "p2p_malloc");
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      cuda_check(e, "p2p_malloc: cudaIpcGetMemHandle");
+    }
+    std::memcpy(out_handle, &h, sizeof(h));
+    *out_ptr = p;
+  });
+}
+magiplan_status magiplan_p2p_free(void* ptr) {
+  MAGI_REQUIRE(ptr);
+  return guarded([&] { cuda_check(cudaFree(ptr), "p2p_free"); });
+}
+magiplan_status magiplan_p2p_open(const unsigned char* handle, void** out_ptr) {
+  MAGI_REQUIRE(handle && out_ptr);
+  return guarded([&] {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    cuda_check(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "p2p_open");
+    *out_ptr = p;
+  });
+}
+magiplan_status magiplan_p2p_close(void* ptr) {
+  MAGI_REQUIRE(ptr);
+  return guarded([&] { cuda_check(cudaIpcCloseMemHandle(ptr), "p2p_close"); });
+}
+magiplan_status magiplan_range_copy_to(const void* src, const int64_t* ranges, const int64_t* offsets,
+                                       const uint64_t* dst_base, const int64_t* dst_row, int64_t num_ranges,
+                                       int64_t total_rows, int64_t row_bytes, void* cuda_stream) {
+  MAGI_REQUIRE(src && (num_ranges == 0 || (ranges && offsets && dst_base && dst_row)));
+  return guarded([&] {
+    if (num_ranges < 0 || total_rows < 0 || row_bytes <= 0 || row_bytes % 16 != 0) {
+      throw UsageError("range_copy_to: row_bytes must be a positive multiple of 16");
+    }
+    cuda_check(magi::launch_range_copy_to(src, ranges, offsets,
+                                          reinterpret_cast<const unsigned long long*>(dst_base), dst_row,
+                                          num_ranges, total_rows, row_bytes, as_stream(cuda_stream)),
+               "range_copy_to launch");
+  });
+}
+magiplan_status magiplan_flags_signal(const uint64_t* flag_ptrs, int32_t n, uint32_t value, void* cuda_stream) {
+  MAGI_REQUIRE(n == 0 || flag_ptrs);
+  return guarded([&] {
+    if (n < 0 || n > 32) throw UsageError("flags_signal: 0 <= n <= 32");
+    cuda_check(magi::launch_flags_signal(reinterpret_cast<unsigned int* const*>(flag_ptrs), n, value,
+                                         as_stream(cuda_stream)),
+               "flags_signal launch");
+  });
+}
+magiplan_status magiplan_flags_wait(const uint32_t* flags, uint32_t mask, uint32_t value, void* cuda_stream) {
+  MAGI_REQUIRE(mask == 0 || flags);
+  return guarded([&] {
+    cuda_check(magi::launch_flags_wait(flags, mask, value, as_stream(cuda_stream)), "flags_wait launch");
   });
 }
 

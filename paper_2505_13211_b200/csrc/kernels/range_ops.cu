@@ -136,6 +136,64 @@ __global__ void range_scatter_add_rows_kernel(const float4* __restrict__ src, fl
   }
 }
 
+// Range copy to per-range destinations (the peer-memory GroupCast): range i
+// sends source rows [ranges[2i], ranges[2i+1]) to dst_base[i] + dst_row[i]
+// rows. Row per warp as in range_gather_rows_kernel; the destinations are
+// other GPUs' receive buffers mapped through CUDA IPC, so the stores travel
+// over NVLink straight into the consumers' buffers (no send staging buffer).
+__global__ void range_copy_to_kernel(const uint4* __restrict__ src, const int64_t* __restrict__ ranges,
+                                     const int64_t* __restrict__ offsets,
+                                     const unsigned long long* __restrict__ dst_base,
+                                     const int64_t* __restrict__ dst_row, int64_t n, int64_t total_rows,
+                                     int64_t vec_per_row) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; r < total_rows;
+       r += warps) {
+    const int64_t j = find_range(offsets, n, r);
+    const int64_t within = r - offsets[j];
+    const uint4* s = src + (ranges[2 * j] + within) * vec_per_row;
+    uint4* d = reinterpret_cast<uint4*>(dst_base[j]) + (dst_row[j] + within) * vec_per_row;
+    for (int64_t c0 = 0; c0 < vec_per_row; c0 += 32 * kRowUnroll) {
+      uint4 v[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) v[u] = s[c];
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) d[c] = v[u];
+      }
+    }
+  }
+}
+
+// Flag protocol of the peer-memory exchange: a release store of `value` to
+// each of n (possibly peer-mapped) flags, after every earlier write of this
+// stream is visible system-wide; and an acquire spin of one thread per set
+// bit of `mask` until local flags[i] >= value.
+__global__ void flags_signal_kernel(unsigned int* const* __restrict__ flags, int n, unsigned int value) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags[i]), "r"(value) : "memory");
+  }
+}
+__global__ void flags_wait_kernel(const unsigned int* __restrict__ flags, unsigned int mask, unsigned int value) {
+  const int i = threadIdx.x;
+  if (i < 32 && ((mask >> i) & 1u)) {
+    unsigned int v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+      if (v >= value) break;
+      __nanosleep(128);
+    }
+  }
+  __syncthreads();
+}
+
 __global__ void cast_kernel(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n4;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -241,6 +299,29 @@ cudaError_t launch_range_gather(const void* src, void* dst, const int64_t* range
         static_cast<const uint4*>(src), static_cast<uint4*>(dst), ranges, offsets, num_ranges,
         total_rows, vec);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_range_copy_to(const void* src, const int64_t* ranges, const int64_t* offsets,
+                                 const unsigned long long* dst_base, const int64_t* dst_row, int64_t num_ranges,
+                                 int64_t total_rows, int64_t row_bytes, cudaStream_t stream) {
+  if (num_ranges == 0 || total_rows == 0) return cudaSuccess;
+  range_copy_to_kernel<<<grid_for(total_rows * 32, 256), 256, 0, stream>>>(
+      static_cast<const uint4*>(src), ranges, offsets, dst_base, dst_row, num_ranges, total_rows,
+      row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flags_signal(unsigned int* const* flags, int n, unsigned int value, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  flags_signal_kernel<<<1, 32, 0, stream>>>(flags, n, value);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_flags_wait(const unsigned int* flags, unsigned int mask, unsigned int value,
+                              cudaStream_t stream) {
+  if (mask == 0) return cudaSuccess;
+  flags_wait_kernel<<<1, 32, 0, stream>>>(flags, mask, value);
   return cudaGetLastError();
 }
 

@@ -89,7 +89,8 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode, stages, check
             S = cpa.xplan["seqlen"]
             nst = (cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"])
         else:
-            cpa = CPAttention(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d)
+            cpa = CPAttention(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d,
+                              transport="p2p" if mode == "p2p" else "nccl")
             S = cpa.xplan["seqlen"]
             nst = (cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"])
         Q, K, V, DO = _inputs(S, hq, hk, d, dev if check == "dense" else "cpu")
@@ -188,6 +189,11 @@ CASES = [
     ("capi", BC4096, 256, 3),
     ("capi", VARLEN, 128, 4),
     ("capi", CAUSAL, 192, None),
+    # the forward GroupCast over NVLink peer memory (IPC-mapped receive
+    # buffers, one range-copy kernel, stream-side flags) instead of NCCL
+    ("p2p", BC4096, 256, 3),
+    ("p2p", VARLEN, 128, None),
+    ("p2p", CAUSAL, 192, 2),
     # ring-attention baseline (zigzag dispatch, K/V around the ring)
     ("ring", BC4096, 0, None),
     ("ring", {"seqlen": 4096, "pattern": "causal"}, 0, None),
@@ -201,8 +207,8 @@ CASES = [
 @pytest.mark.parametrize("mode,mask,chunk,stages", CASES,
                          ids=[f"{m}-{k['pattern']}-{k['seqlen']}-s{s}" for m, k, _, s in CASES])
 def test_cp_matches_oracle(built_lib, cuda, world, mode, mask, chunk, stages):
-    if torch.cuda.device_count() < world and mode == "capi":
-        pytest.skip(f"the C-ABI executor speaks NCCL, one rank per GPU: needs {world} GPUs")
+    if torch.cuda.device_count() < world and mode in ("capi", "p2p"):
+        pytest.skip(f"{mode}: one rank per GPU, needs {world} GPUs")
     from oracle import oracle
     from paper_2505_13211_b200.planner import Mask
 
