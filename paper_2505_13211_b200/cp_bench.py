@@ -140,7 +140,7 @@ def run(args) -> None:
 
         cpa = CPExecutorC(scenario(world), HQ, HK, D)
     else:
-        cpa = CPAttention(scenario(world), HQ, HK, D)
+        cpa = CPAttention(scenario(world), HQ, HK, D, transport="p2p" if mode == "p2p" else "nccl")
     L = cpa.local_tokens
     g = torch.Generator(device="cpu").manual_seed(1234 + rank)
     q_h = torch.randn(L, HQ, D, generator=g).to(torch.bfloat16).pin_memory()
@@ -263,7 +263,8 @@ def run(args) -> None:
             n_launch = 2 + 3 * nf + 1 + 3 + 4 * nb + 2 * world * nb + 3
         else:
             for st in cpa.fwd_stages:
-                n_launch += 1 + 2 * (1 if sum(st.send_splits) else 0)
+                # p2p: flag wait + 2 copies + signal on the comm stream, wait + signal beside the FFA
+                n_launch += 1 + (6 if mode == "p2p" else 2 * (1 if sum(st.send_splits) else 0))
             for st in cpa.bwd_stages:
                 n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
             n_launch += 2 + 1 + 2 + 3  # host fwd + cast, preprocess, host bwd (2), final casts
