@@ -230,6 +230,15 @@ MAGIPLAN_API magiplan_status magiplan_range_copy_to(const void* src, const int64
                                                     const int64_t* dst_row, int64_t num_ranges,
                                                     int64_t total_rows, int64_t row_bytes,
                                                     void* cuda_stream);
+/* Range Scatter-Reduce fused with the transfer: dst rows [ranges[2i],
+ * ranges[2i+1]) += rows src_row[i].. of the f32 buffer at src_base[i]
+ * (device arrays; bases may be peer-mapped). One call per source rank, in
+ * rank order, keeps sums deterministic. */
+MAGIPLAN_API magiplan_status magiplan_range_scatter_add_from(float* dst, const int64_t* ranges,
+                                                             const int64_t* offsets, const uint64_t* src_base,
+                                                             const int64_t* src_row, int64_t num_ranges,
+                                                             int64_t total_rows, int64_t row_elems,
+                                                             void* cuda_stream);
 /* Stream-ordered flags: a system-scope release store of `value` to each of
  * the n <= 32 flags whose addresses are in the device array flag_ptrs; and a
  * wait until flags[i] >= value for every set bit i of mask (acquire). */

@@ -61,6 +61,7 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_p2p_open": (C.c_int, [C.c_char_p, C.POINTER(C.c_void_p)]),
     "magiplan_p2p_close": (C.c_int, [_vp]),
     "magiplan_range_copy_to": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "magiplan_range_scatter_add_from": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
     "magiplan_flags_signal": (C.c_int, [_vp, _i32, C.c_uint32, _vp]),
     "magiplan_flags_wait": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _vp]),
     "magiplan_debug_umma_tile": (C.c_int, [_vp, _vp, _vp, _i32, _vp]),

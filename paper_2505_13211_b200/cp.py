@@ -164,7 +164,9 @@ class CPAttention:
         self.L = _lib.lib()
         self.timeline: list | None = None  # set to [] to record per-stage CUDA events
         self._p2p: list[dict] = []
+        self._p2p_bwd: list[dict] = []
         self._p2p_epoch = 0
+        self._p2p_bepoch = 0
         self._p2p_owned: list[int] = []
         self._p2p_opened: list[int] = []
         if transport == "p2p" and self.world > 1:
@@ -172,11 +174,15 @@ class CPAttention:
 
     # ------------------------------------------------------------ peer memory
     def _setup_p2p(self):
-        """Per forward stage: receive buffers and a flag block [ready[cp] |
-        consumed[cp]] in IPC-exportable memory, handles exchanged once, the
-        peers' buffers mapped, and the device arrays of the fused
-        gather-and-send kernel built from the executor plan (every
-        consumer's receive entries from this rank, at their buffer rows)."""
+        """Per stage of both passes: receive buffers and a flag block in
+        IPC-exportable memory, handles exchanged once, the peers' buffers
+        mapped, and the device arrays of the fused gather-and-send kernel
+        built from the executor plan (every consumer's receive entries from
+        this rank, at their buffer rows). Backward stages also get f32
+        partial dK / dV buffers the owners read back for the GroupReduce.
+        Flag block of a stage (uint32, index = peer rank): [ready | consumed
+        | partials ready | partials read], each written by the peer into this
+        rank's block."""
         import ctypes as C
 
         cp, me, L = self.world, self.rank, self.L
@@ -190,73 +196,109 @@ class CPAttention:
             self._p2p_owned.append(ptr.value)
             return ptr.value, h.raw
 
-        def view(ptr, n, dtype):
+        def view(ptr, n, typestr, dtype):
             class _Raw:
-                __cuda_array_interface__ = {"shape": (n,), "typestr": "<i2" if dtype == torch.bfloat16 else "<i4",
-                                            "data": (ptr, False), "version": 3, "strides": None}
-            t = torch.as_tensor(_Raw(), device=self.device)
-            return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
+                __cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                            "version": 3, "strides": None}
+            return torch.as_tensor(_Raw(), device=self.device).view(dtype)
 
+        def dev64(vals):
+            return torch.tensor(vals if vals else [0], dtype=torch.int64, device=self.device)
+
+        ranks = self.xplan["ranks"]
+        passes = (("fwd_stages", self.fwd_stages, False), ("bwd_stages", self.bwd_stages, True))
         local, handles = [], []
-        for st in self.fwd_stages:
-            n = max(st.buf_tokens, 1) * self.hk * self.d
-            kp, kh = alloc(n * 2)
-            vp, vh = alloc(n * 2)
-            fp, fh = alloc(2 * cp * 4)
-            view(fp, 2 * cp, torch.int32).zero_()
-            local.append((kp, vp, fp))
-            handles.append((kh, vh, fh))
+        for _key, stages, bwd in passes:
+            for st in stages:
+                n = max(st.buf_tokens, 1) * self.hk * self.d
+                bufs = [alloc(n * 2), alloc(n * 2)]           # K, V receive buffers (bf16)
+                if bwd:
+                    bufs += [alloc(n * 4), alloc(n * 4)]      # partial dK, dV (f32)
+                fp, fh = alloc(4 * cp * 4)
+                view(fp, 4 * cp, "<i4", torch.int32).zero_()
+                local.append(([b[0] for b in bufs], fp))
+                handles.append(([b[1] for b in bufs], fh))
         torch.cuda.synchronize(self.device)
         every = [None] * cp
         dist.all_gather_object(every, handles, group=self.group)
-        ranks = self.xplan["ranks"]
 
-        def dev64(vals, dtype=torch.int64):
-            return torch.tensor(vals if vals else [0], dtype=dtype, device=self.device)
+        idx = 0
+        for key, stages, bwd in passes:
+            out = []
+            for j, st in enumerate(stages):
+                ptrs, fp = local[idx]
+                peer = {}
+                for d in range(cp):
+                    if d == me:
+                        continue
+                    hb, hf = every[d][idx]
+                    opened = []
+                    for h in hb + [hf]:
+                        o = C.c_void_p()
+                        _lib.check(L.magiplan_p2p_open(h, C.byref(o)))
+                        self._p2p_opened.append(o.value)
+                        opened.append(o.value)
+                    peer[d] = opened          # [k, v, (dk, dv,) flags]
+                idx += 1
+                ranges, offs, kbase, vbase, drow, acc = [], [], [], [], [], 0
+                dests, per_dst = [], {}
+                for d in range(cp):
+                    if d == me or j >= len(ranks[d][key]):
+                        continue
+                    mine = [e for e in ranks[d][key][j]["recv"] if e[0] == me]
+                    if not mine:
+                        continue
+                    dests.append(d)
+                    rr, ro, rb_dk, rb_dv, rrow, racc = [], [], [], [], [], 0
+                    for _src, gs, ge, src_local, buf_off in mine:
+                        ranges += [src_local, src_local + (ge - gs)]
+                        offs.append(acc)
+                        acc += ge - gs
+                        kbase.append(peer[d][0])
+                        vbase.append(peer[d][1])
+                        drow.append(buf_off)
+                        if bwd:
+                            rr += [src_local, src_local + (ge - gs)]
+                            ro.append(racc)
+                            racc += ge - gs
+                            rb_dk.append(peer[d][2])
+                            rb_dv.append(peer[d][3])
+                            rrow.append(buf_off)
+                    if bwd:
+                        per_dst[d] = (dev64(rr), dev64(ro), dev64(rb_dk), dev64(rb_dv), dev64(rrow),
+                                      len(ro), racc)
+                srcs = sorted({e[0] for e in ranks[me][key][j]["recv"]}) if j < len(ranks[me][key]) else []
+                nt = max(st.buf_tokens, 1) * self.hk * self.d
+                P = {
+                    "kb": view(ptrs[0], nt, "<i2", torch.bfloat16).view(-1, self.hk, self.d)[:st.buf_tokens],
+                    "vb": view(ptrs[1], nt, "<i2", torch.bfloat16).view(-1, self.hk, self.d)[:st.buf_tokens],
+                    "flags": fp, "rows": acc, "n": len(offs), "row_bytes": row,
+                    "ranges": dev64(ranges), "offs": dev64(offs), "drow": dev64(drow),
+                    "kbase": dev64(kbase), "vbase": dev64(vbase),
+                    # cast: producer raises consumers' ready[me], waits its own consumed[d]
+                    "sig_send": dev64([peer[d][-1] + 4 * me for d in dests]), "n_dest": len(dests),
+                    "mask_dest": sum(1 << d for d in dests),
+                    "sig_recv": dev64([peer[s_][-1] + 4 * (cp + me) for s_ in srcs]), "n_src": len(srcs),
+                    "mask_src": sum(1 << s_ for s_ in srcs),
+                }
+                if bwd:
+                    P["dkb"] = view(ptrs[2], nt, "<f4", torch.float32).view(-1, self.hk, self.d)[:st.buf_tokens]
+                    P["dvb"] = view(ptrs[3], nt, "<f4", torch.float32).view(-1, self.hk, self.d)[:st.buf_tokens]
+                    # reduce: consumer raises owners' pready[me]; owner raises consumers' pdone[me]
+                    P["sig_pready"] = dev64([peer[s_][-1] + 4 * (2 * cp + me) for s_ in srcs])
+                    P["sig_pdone"] = dev64([peer[d][-1] + 4 * (3 * cp + me) for d in dests])
+                    P["per_dst"] = per_dst
+                out.append(P)
+            if bwd:
+                self._p2p_bwd = out
+            else:
+                self._p2p = out
 
-        for j, st in enumerate(self.fwd_stages):
-            kp, vp, fp = local[j]
-            peer = {}
-            for d in range(cp):
-                if d == me:
-                    continue
-                ptrs = []
-                for h in every[d][j]:
-                    out = C.c_void_p()
-                    _lib.check(L.magiplan_p2p_open(h, C.byref(out)))
-                    self._p2p_opened.append(out.value)
-                    ptrs.append(out.value)
-                peer[d] = ptrs
-            ranges, offs, kbase, vbase, drow, sig_send, wait_send = [], [], [], [], [], [], 0
-            acc = 0
-            for d in range(cp):
-                if d == me or j >= len(ranks[d]["fwd_stages"]):
-                    continue
-                mine = [e for e in ranks[d]["fwd_stages"][j]["recv"] if e[0] == me]
-                for _src, gs, ge, src_local, buf_off in mine:
-                    ranges += [src_local, src_local + (ge - gs)]
-                    offs.append(acc)
-                    acc += ge - gs
-                    kbase.append(peer[d][0])
-                    vbase.append(peer[d][1])
-                    drow.append(buf_off)
-                if mine:
-                    sig_send.append(peer[d][2] + 4 * me)      # d's ready[me]
-                    wait_send |= 1 << d                        # my consumed[d]
-            srcs = sorted({e[0] for e in ranks[me]["fwd_stages"][j]["recv"]})
-            self._p2p.append({
-                "kb": view(kp, max(st.buf_tokens, 1) * self.hk * self.d, torch.bfloat16)
-                .view(-1, self.hk, self.d)[:st.buf_tokens],
-                "vb": view(vp, max(st.buf_tokens, 1) * self.hk * self.d, torch.bfloat16)
-                .view(-1, self.hk, self.d)[:st.buf_tokens],
-                "flags": fp, "rows": acc, "n": len(offs), "row_bytes": row,
-                "ranges": dev64(ranges), "offs": dev64(offs), "drow": dev64(drow),
-                "kbase": dev64(kbase), "vbase": dev64(vbase),
-                "sig_send": dev64(sig_send), "n_sig_send": len(sig_send), "wait_send": wait_send,
-                "wait_recv": sum(1 << s_ for s_ in srcs),
-                "sig_recv": dev64([peer[s_][2] + 4 * (cp + me) for s_ in srcs]),
-                "n_sig_recv": len(srcs),
-            })
+    def _flags_wait(self, P, block: int, mask: int, value: int, stream):
+        _lib.check(self.L.magiplan_flags_wait(P["flags"] + 4 * block * self.world, mask, value, stream.cuda_stream))
+
+    def _flags_signal(self, ptrs, n: int, value: int, stream):
+        _lib.check(self.L.magiplan_flags_signal(ptrs.data_ptr(), n, value, stream.cuda_stream))
 
     def close(self):
         """Release the peer-memory mappings and buffers (p2p transport)."""
@@ -267,25 +309,41 @@ class CPAttention:
             self.L.magiplan_p2p_close(ptr)
         for ptr in self._p2p_owned:
             self.L.magiplan_p2p_free(ptr)
-        self._p2p_opened, self._p2p_owned, self._p2p = [], [], []
+        self._p2p_opened, self._p2p_owned, self._p2p, self._p2p_bwd = [], [], [], []
 
-    def _cast_p2p(self, j: int, k: torch.Tensor, v: torch.Tensor):
-        """Forward GroupCast of stage j over peer memory, on the comm stream:
-        wait until every consumer has released this stage's buffer from the
+    def _cast_p2p(self, P: dict, epoch: int, k: torch.Tensor, v: torch.Tensor):
+        """GroupCast of one stage over peer memory, on the comm stream: wait
+        until every consumer has released this stage's buffer from the
         previous pass, copy the ranges into the consumers' buffers, then
         raise their ready flags. Same return shape as _cast."""
-        P, L, e = self._p2p[j], self.L, self._p2p_epoch
+        L = self.L
         sp = self.comm_stream.cuda_stream
         with torch.cuda.stream(self.comm_stream):
             e0 = self._ev(self.comm_stream)
-            _lib.check(L.magiplan_flags_wait(P["flags"] + 4 * self.world, P["wait_send"], e - 1, sp))
+            self._flags_wait(P, 1, P["mask_dest"], epoch - 1, self.comm_stream)
             if P["n"]:
                 for src, base in ((k, P["kbase"]), (v, P["vbase"])):
                     _lib.check(L.magiplan_range_copy_to(src.data_ptr(), P["ranges"].data_ptr(),
                                                         P["offs"].data_ptr(), base.data_ptr(), P["drow"].data_ptr(),
                                                         P["n"], P["rows"], P["row_bytes"], sp))
-            _lib.check(L.magiplan_flags_signal(P["sig_send"].data_ptr(), P["n_sig_send"], e, sp))
+            self._flags_signal(P["sig_send"], P["n_dest"], epoch, self.comm_stream)
         return P["kb"], P["vb"], [], None, e0
+
+    def _reduce_p2p(self, P: dict, epoch: int, dk, dv):
+        """GroupReduce of one backward stage over peer memory, on the reduce
+        stream: wait for the consumers' partials, then per consumer in rank
+        order add its partial dK / dV rows (read over NVLink) into this
+        rank's dK / dV, then tell it the buffers may be reused."""
+        rs = self.reduce_stream
+        self._flags_wait(P, 2, P["mask_dest"], epoch, rs)
+        row_elems = self.hk * self.d
+        for d in sorted(P["per_dst"]):
+            rr, ro, bdk, bdv, rrow, n, rows = P["per_dst"][d]
+            for acc, base in ((dk, bdk), (dv, bdv)):
+                _lib.check(self.L.magiplan_range_scatter_add_from(
+                    acc.data_ptr(), rr.data_ptr(), ro.data_ptr(), base.data_ptr(), rrow.data_ptr(), n, rows,
+                    row_elems, rs.cuda_stream))
+        self._flags_signal(P["sig_pdone"], P["n_dest"], epoch, rs)
 
     # ------------------------------------------------------------ tracing
     def _ev(self, stream):
@@ -405,7 +463,8 @@ class CPAttention:
         p2p = bool(self._p2p)
         if p2p:
             self._p2p_epoch += 1
-        cast = (lambda j: self._cast_p2p(j, k, v)) if p2p else (lambda j: self._cast(self.fwd_stages[j], k, v))
+        cast = ((lambda j: self._cast_p2p(self._p2p[j], self._p2p_epoch, k, v)) if p2p
+                else (lambda j: self._cast(self.fwd_stages[j], k, v)))
         # step 0: cast(1) is issued first, then the host-local FFA
         pending = cast(0) if self.fwd_stages else None
         e0 = self._ev(cur)
@@ -425,7 +484,7 @@ class CPAttention:
             if p2p:
                 # the peers' copies into this rank's buffer have landed
                 P = self._p2p[j]
-                _lib.check(self.L.magiplan_flags_wait(P["flags"], P["wait_recv"], self._p2p_epoch, cur.cuda_stream))
+                self._flags_wait(P, 0, P["mask_src"], self._p2p_epoch, cur)
                 if self.timeline is not None:
                     self._span("fwd", "cast", j + 1, ec, self._ev(cur))
             else:
@@ -436,8 +495,7 @@ class CPAttention:
             self._span("fwd", "ffa", j + 1, e0, self._ev(cur))
             if p2p:
                 # release the buffer: the producers may overwrite it next pass
-                _lib.check(self.L.magiplan_flags_signal(P["sig_recv"].data_ptr(), P["n_sig_recv"],
-                                                        self._p2p_epoch, cur.cuda_stream))
+                self._flags_signal(P["sig_recv"], P["n_src"], self._p2p_epoch, cur)
         out_bf = torch.empty((L, self.hq, self.d), dtype=torch.bfloat16, device=q.device)
         _lib.check(self.L.magiplan_cast_f32_bf16(out.data_ptr(), out_bf.data_ptr(), out.numel(),
                                                  cur.cuda_stream))
@@ -460,8 +518,14 @@ class CPAttention:
         dv = torch.empty_like(dk)
         self.comm_stream.wait_stream(cur)
         keep = []
+        p2p = bool(self._p2p_bwd)
+        if p2p:
+            self._p2p_bepoch += 1
+        eb = self._p2p_bepoch
+        cast = ((lambda j: self._cast_p2p(self._p2p_bwd[j], eb, k, v)) if p2p
+                else (lambda j: self._cast(self.bwd_stages[j], k, v)))
         # step 0: cast(1) first, then preprocess + host-local dQ / dK / dV
-        pending = self._cast(self.bwd_stages[0], k, v) if self.bwd_stages else None
+        pending = cast(0) if self.bwd_stages else None
         e0 = self._ev(cur)
         _lib.check(Ld.magiplan_ffa_bwd_preprocess(out_f32.data_ptr(), dout.data_ptr(),
                                                   delta.data_ptr(), L, self.hq, self.d, _lib.F32, sp))
@@ -480,12 +544,20 @@ class CPAttention:
             # step j+1: cast(j+2) || ffa(j+1) || reduce(j), the reduce having
             # been issued on its own stream right after ffa(j)
             if j + 1 < len(self.bwd_stages):
-                pending = self._cast(self.bwd_stages[j + 1], k, v)
-            self._cast_done("bwd", j + 1, works, ec)
-            # the dK/dV pass writes every row of its partial buffers (keys no
-            # slice reaches get zeros), so they need no initialisation
-            dkb = torch.empty((st.buf_tokens, self.hk, self.d), dtype=torch.float32, device=dev)
-            dvb = torch.empty_like(dkb)
+                pending = cast(j + 1)
+            if p2p:
+                P = self._p2p_bwd[j]
+                # the peers' K / V for this stage have landed, and the owners
+                # have read last pass's partials out of dkb / dvb
+                self._flags_wait(P, 0, P["mask_src"], eb, cur)
+                self._flags_wait(P, 3, P["mask_src"], eb - 1, cur)
+                dkb, dvb = P["dkb"], P["dvb"]
+            else:
+                self._cast_done("bwd", j + 1, works, ec)
+                # the dK/dV pass writes every row of its partial buffers (keys no
+                # slice reaches get zeros), so they need no initialisation
+                dkb = torch.empty((st.buf_tokens, self.hk, self.d), dtype=torch.float32, device=dev)
+                dvb = torch.empty_like(dkb)
             e0 = self._ev(cur)
             if st.plan is not None:
                 # fresh partial dK/dV of the received keys; dQ added into the
@@ -498,11 +570,20 @@ class CPAttention:
                 dkb.zero_()
                 dvb.zero_()
             self._span("bwd", "ffa", j + 1, e0, self._ev(cur))
+            if p2p:
+                # release this stage's K / V buffer, publish the partials
+                self._flags_signal(P["sig_recv"], P["n_src"], eb, cur)
+                self._flags_signal(P["sig_pready"], P["n_src"], eb, cur)
             self.reduce_stream.wait_stream(cur)  # partial dK/dV of this stage (and dk/dv) ready
             er = self._ev(self.reduce_stream)
-            recv = self._reduce(st, dkb, dvb, dk, dv)
+            if p2p:
+                self._reduce_p2p(P, eb, dk, dv)
+                recv = None
+            else:
+                recv = self._reduce(st, dkb, dvb, dk, dv)
             self._span("bwd", "reduce", j + 1, er, self._ev(self.reduce_stream))
-            keep.append((kb, vb, sent, dkb, dvb, recv))
+            if not p2p:
+                keep.append((kb, vb, sent, dkb, dvb, recv))
         cur.wait_stream(self.reduce_stream)
         outs = []
         for t in (dq, dk, dv):

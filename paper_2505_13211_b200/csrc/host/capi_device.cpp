@@ -32,6 +32,10 @@ cudaError_t launch_range_copy_to(const void* src, const int64_t* ranges, const i
                                  const unsigned long long* dst_base, const int64_t* dst_row, int64_t num_ranges,
                                  int64_t total_rows, int64_t row_bytes, cudaStream_t stream);
 cudaError_t launch_flags_signal(unsigned int* const* flags, int n, unsigned int value, cudaStream_t stream);
+cudaError_t launch_range_scatter_add_from(float* dst, const int64_t* ranges, const int64_t* offsets,
+                                          const unsigned long long* src_base, const int64_t* src_row,
+                                          int64_t num_ranges, int64_t total_rows, int64_t row_elems,
+                                          cudaStream_t stream);
 cudaError_t launch_flags_wait(const unsigned int* flags, unsigned int mask, unsigned int value,
                               cudaStream_t stream);
 cudaError_t launch_range_gather(const void* src, void* dst, const int64_t* ranges,
@@ -331,6 +335,21 @@ magiplan_status magiplan_range_copy_to(const void* src, const int64_t* ranges, c
                                           reinterpret_cast<const unsigned long long*>(dst_base), dst_row,
                                           num_ranges, total_rows, row_bytes, as_stream(cuda_stream)),
                "range_copy_to launch");
+  });
+}
+magiplan_status magiplan_range_scatter_add_from(float* dst, const int64_t* ranges, const int64_t* offsets,
+                                                const uint64_t* src_base, const int64_t* src_row,
+                                                int64_t num_ranges, int64_t total_rows, int64_t row_elems,
+                                                void* cuda_stream) {
+  MAGI_REQUIRE(dst && (num_ranges == 0 || (ranges && offsets && src_base && src_row)));
+  return guarded([&] {
+    if (num_ranges < 0 || total_rows < 0 || row_elems <= 0 || row_elems % 4 != 0) {
+      throw UsageError("range_scatter_add_from: row_elems must be a positive multiple of 4");
+    }
+    cuda_check(magi::launch_range_scatter_add_from(dst, ranges, offsets,
+                                                   reinterpret_cast<const unsigned long long*>(src_base), src_row,
+                                                   num_ranges, total_rows, row_elems, as_stream(cuda_stream)),
+               "range_scatter_add_from launch");
   });
 }
 magiplan_status magiplan_flags_signal(const uint64_t* flag_ptrs, int32_t n, uint32_t value, void* cuda_stream) {

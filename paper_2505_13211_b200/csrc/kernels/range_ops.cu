@@ -170,6 +170,43 @@ __global__ void range_copy_to_kernel(const uint4* __restrict__ src, const int64_
   }
 }
 
+// Scatter-add from per-range sources (the peer-memory GroupReduce): range i
+// adds rows src_base[i] + src_row[i].. (f32, possibly a peer's buffer read
+// over NVLink) into dst rows [ranges[2i], ranges[2i+1]). One call per
+// source rank in rank order keeps the sums deterministic; a call's ranges
+// never alias.
+__global__ void range_scatter_add_from_kernel(float4* __restrict__ dst, const int64_t* __restrict__ ranges,
+                                              const int64_t* __restrict__ offsets,
+                                              const unsigned long long* __restrict__ src_base,
+                                              const int64_t* __restrict__ src_row, int64_t n, int64_t total_rows,
+                                              int64_t vec_per_row) {
+  const int lane = threadIdx.x % 32;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
+  for (int64_t r = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32; r < total_rows;
+       r += warps) {
+    const int64_t j = find_range(offsets, n, r);
+    const int64_t within = r - offsets[j];
+    float4* d = dst + (ranges[2 * j] + within) * vec_per_row;
+    const float4* s = reinterpret_cast<const float4*>(src_base[j]) + (src_row[j] + within) * vec_per_row;
+    for (int64_t c0 = 0; c0 < vec_per_row; c0 += 32 * kRowUnroll) {
+      float4 a[kRowUnroll], b[kRowUnroll];
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) {
+          a[u] = d[c];
+          b[u] = s[c];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kRowUnroll; ++u) {
+        const int64_t c = c0 + u * 32 + lane;
+        if (c < vec_per_row) d[c] = make_float4(a[u].x + b[u].x, a[u].y + b[u].y, a[u].z + b[u].z, a[u].w + b[u].w);
+      }
+    }
+  }
+}
+
 // Flag protocol of the peer-memory exchange: a release store of `value` to
 // each of n (possibly peer-mapped) flags, after every earlier write of this
 // stream is visible system-wide; and an acquire spin of one thread per set
@@ -309,6 +346,16 @@ cudaError_t launch_range_copy_to(const void* src, const int64_t* ranges, const i
   range_copy_to_kernel<<<grid_for(total_rows * 32, 256), 256, 0, stream>>>(
       static_cast<const uint4*>(src), ranges, offsets, dst_base, dst_row, num_ranges, total_rows,
       row_bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_range_scatter_add_from(float* dst, const int64_t* ranges, const int64_t* offsets,
+                                          const unsigned long long* src_base, const int64_t* src_row,
+                                          int64_t num_ranges, int64_t total_rows, int64_t row_elems,
+                                          cudaStream_t stream) {
+  if (num_ranges == 0 || total_rows == 0) return cudaSuccess;
+  range_scatter_add_from_kernel<<<grid_for(total_rows * 32, 256), 256, 0, stream>>>(
+      reinterpret_cast<float4*>(dst), ranges, offsets, src_base, src_row, num_ranges, total_rows, row_elems / 4);
   return cudaGetLastError();
 }
 

@@ -192,6 +192,7 @@ CASES = [
     # the forward GroupCast over NVLink peer memory (IPC-mapped receive
     # buffers, one range-copy kernel, stream-side flags) instead of NCCL
     ("p2p", BC4096, 256, 3),
+    ("p2p", BC4096, 256, None),
     ("p2p", VARLEN, 128, None),
     ("p2p", CAUSAL, 192, 2),
     # ring-attention baseline (zigzag dispatch, K/V around the ring)
