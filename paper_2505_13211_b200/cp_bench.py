@@ -265,8 +265,14 @@ def run(args) -> None:
             for st in cpa.fwd_stages:
                 # p2p: flag wait + 2 copies + signal on the comm stream, wait + signal beside the FFA
                 n_launch += 1 + (6 if mode == "p2p" else 2 * (1 if sum(st.send_splits) else 0))
-            for st in cpa.bwd_stages:
-                n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
+            if mode == "p2p":
+                # per stage: cast (wait, 2 copies, signal), compute (2 waits, dK/dV + dQ, 2 signals),
+                # reduce (wait, 2 scatter-adds per consumer, signal)
+                for P in cpa._p2p_bwd:
+                    n_launch += 4 + 6 + 2 + 2 * len(P["per_dst"])
+            else:
+                for st in cpa.bwd_stages:
+                    n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world
             n_launch += 2 + 1 + 2 + 3  # host fwd + cast, preprocess, host bwd (2), final casts
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
