@@ -1,4 +1,4 @@
-"""Context-parallel FFA at 2 and 4 ranks, checked against the CPU
+"""Context-parallel FFA at 2, 4 and 8 ranks, checked against the CPU
 oracle on the global sequence, and at the SURVEY §8d config-5 reduced shape
 (S = 65536, block-causal 8192, 48 q / 8 kv heads, greedy dispatch with the
 default chunk) against the dense fp32 reference on sampled rows.
@@ -208,6 +208,10 @@ CASES = [
 @pytest.mark.parametrize("mode,mask,chunk,stages", CASES,
                          ids=[f"{m}-{k['pattern']}-{k['seqlen']}-s{s}" for m, k, _, s in CASES])
 def test_cp_matches_oracle(built_lib, cuda, world, mode, mask, chunk, stages):
+    _check_vs_oracle(world, mode, mask, chunk, stages)
+
+
+def _check_vs_oracle(world, mode, mask, chunk, stages):
     if torch.cuda.device_count() < world and mode in ("capi", "p2p"):
         pytest.skip(f"{mode}: one rank per GPU, needs {world} GPUs")
     from oracle import oracle
@@ -262,6 +266,37 @@ def test_cp_config5_reduced(built_lib, cuda, world, stages):
         assert same
         if stages == 3:
             assert max(nst) > 1, nst
+        assert errs["O"][1] < O_REL and errs["LSE"][0] < LSE_ABS, errs
+        for nm in ("dQ", "dK", "dV"):
+            assert errs[nm][1] < G_REL, (nm, errs)
+
+
+W8_CASES = [
+    ("magi", BC4096, 128, 3),
+    ("magi", CAUSAL, 96, None),
+    ("ring", BC4096, 0, None),
+]
+
+
+@pytest.mark.parametrize("mode,mask,chunk,stages", W8_CASES,
+                         ids=[f"{m}-{k['pattern']}-{k['seqlen']}-s{s}" for m, k, _, s in W8_CASES])
+def test_cp_world8_matches_oracle(built_lib, cuda, mode, mask, chunk, stages):
+    """cp = 8 (the 1M-token scaling point's rank count; its bench plan has a
+    2-stage backward): 8 ranks, one per GPU on an 8-GPU box, otherwise
+    sharing the GPUs over gloo; every rank's rows checked against the oracle."""
+    _check_vs_oracle(8, mode, mask, chunk, stages)
+
+
+@pytest.mark.parametrize("stages", [2])
+def test_cp_world8_config5_reduced(built_lib, cuda, stages):
+    """The config-5 reduced shape at cp = 8 with a forced 2-stage split (the
+    bench's cp-8 plan runs a 2-stage backward)."""
+    chunk = 65536 // 8 // 8
+    res = _launch(8, CFG5, chunk, 48, 8, 128, "magi", stages, "dense", next(_PORTS))
+    for rank, nst, same, errs in res:
+        print("config5", 8, stages, rank, nst, {k_: f"abs {a:.2e} rel {b:.2e}" for k_, (a, b) in errs.items()})
+        assert same
+        assert max(nst) > 1, nst
         assert errs["O"][1] < O_REL and errs["LSE"][0] < LSE_ABS, errs
         for nm in ("dQ", "dK", "dV"):
             assert errs[nm][1] < G_REL, (nm, errs)
