@@ -520,10 +520,11 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-weak-anchor", action="store_true",
                     help="N=1: skip the cp=1 run of the CP weak-scaling workload")
-    ap.add_argument("--cp-mode", default="magi", choices=["magi", "p2p", "capi", "ring", "ulysses"],
+    ap.add_argument("--cp-mode", default="magi", choices=["magi", "p2p", "capi", "capi_p2p", "ring", "ulysses"],
                     help="N>1 only: MagiAttention GroupCast CP (default; 'p2p' = the forward GroupCast "
                          "over NVLink peer memory instead of NCCL; 'capi' = the same schedule through the "
-                         "C-ABI executor), or the ring-attention / Ulysses baselines")
+                         "C-ABI executor; 'capi_p2p' = that executor over NVLink peer memory), or the "
+                         "ring-attention / Ulysses baselines")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

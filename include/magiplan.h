@@ -263,9 +263,24 @@ MAGIPLAN_API magiplan_status magiplan_cp_create(const magiplan_scenario* scenari
                                                 const void* nccl_unique_id, int64_t num_heads_q,
                                                 int64_t num_heads_k, int32_t head_dim,
                                                 float softmax_scale, magiplan_cp** out);
+/* Transport of the GroupCast / GroupReduce bytes. NCCL: grouped point-to-point
+ * on two communicators. P2P: NVLink peer memory (one rank per GPU of one
+ * node, cp_size <= 32): the stage buffers are CUDA-IPC memory whose handles
+ * are all-gathered at creation (over the NCCL communicator), the GroupCast
+ * is a fused gather-and-send kernel writing into the consumers' buffers, the
+ * GroupReduce a per-consumer scatter-add (rank order) reading their partials,
+ * ordered by stream-side release / acquire flags. Same results bit for bit. */
+typedef enum magiplan_cp_transport { MAGIPLAN_CP_NCCL = 0, MAGIPLAN_CP_P2P = 1 } magiplan_cp_transport;
+/* magiplan_cp_create with a transport (magiplan_cp_create = MAGIPLAN_CP_NCCL). */
+MAGIPLAN_API magiplan_status magiplan_cp_create_ex(const magiplan_scenario* scenario, int32_t rank,
+                                                   const void* nccl_unique_id, int64_t num_heads_q,
+                                                   int64_t num_heads_k, int32_t head_dim,
+                                                   float softmax_scale, int32_t transport,
+                                                   magiplan_cp** out);
 MAGIPLAN_API void magiplan_cp_free(magiplan_cp* cp);
 /* {"rank","cp_size","local_tokens","chunk_size","chunks":[global chunk ids in
- *  local order],"num_stages_fwd","num_stages_bwd","area_multiplicity"} */
+ *  local order],"num_stages_fwd","num_stages_bwd","area_multiplicity",
+ *  "transport":"nccl"|"p2p"} */
 MAGIPLAN_API magiplan_status magiplan_cp_describe(const magiplan_cp* cp, char** out_json);
 /* Local shards in chunk order: q [L, hq, d], k / v [L, hk, d] bf16; out_f32
  * [L, hq, d] and lse [hq, L] f32 (kept for the backward); out_bf16 optional. */

@@ -49,6 +49,7 @@ SIGNATURES: dict[str, tuple] = {
     "magiplan_ffa_bwd_dq": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _f32, _i32, _i32, _vp]),
     "magiplan_cp_unique_id": (C.c_int, [_vp]),
     "magiplan_cp_create": (C.c_int, [_vp, _i32, _vp, _i64, _i64, _i32, _f32, C.POINTER(_vp)]),
+    "magiplan_cp_create_ex": (C.c_int, [_vp, _i32, _vp, _i64, _i64, _i32, _f32, _i32, C.POINTER(_vp)]),
     "magiplan_cp_free": (None, [_vp]),
     "magiplan_cp_describe": (C.c_int, [_vp, C.POINTER(_vp)]),
     "magiplan_cp_forward": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),

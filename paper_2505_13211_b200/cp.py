@@ -615,8 +615,11 @@ class CPExecutorC:
     broadcast; the executor creates its own NCCL communicators."""
 
     def __init__(self, scenario: dict | str, num_heads_q: int, num_heads_k: int, head_dim: int,
-                 group=None, device=None, softmax_scale: float | None = None):
+                 group=None, device=None, softmax_scale: float | None = None, transport: str = "nccl"):
         import ctypes as C
+
+        if transport not in ("nccl", "p2p"):
+            raise ValueError(f"transport {transport!r}: 'nccl' or 'p2p'")
 
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
@@ -634,14 +637,16 @@ class CPExecutorC:
         self._scen = Scenario(scenario)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
-            _lib.check(self.L.magiplan_cp_create(self._scen._h, self.rank, uid, num_heads_q, num_heads_k, head_dim,
-                                                 self.scale, C.byref(h)))
+            _lib.check(self.L.magiplan_cp_create_ex(self._scen._h, self.rank, uid, num_heads_q, num_heads_k,
+                                                    head_dim, self.scale, 0 if transport == "nccl" else 1,
+                                                    C.byref(h)))
         self._h = h
         out = C.c_void_p()
         _lib.check(self.L.magiplan_cp_describe(self._h, C.byref(out)))
         info = json.loads(_lib.take_string(out))
         self.chunks, self.chunk_size = info["chunks"], info["chunk_size"]
         self.local_tokens = info["local_tokens"]
+        self.transport = info["transport"]
         self.xplan = {"num_stages_fwd": info["num_stages_fwd"], "num_stages_bwd": info["num_stages_bwd"],
                       "area_multiplicity": info["area_multiplicity"], "seqlen": self.local_tokens * self.world}
 

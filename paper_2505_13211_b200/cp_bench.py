@@ -135,10 +135,10 @@ def run(args) -> None:
         from paper_2505_13211_b200.ulysses import UlyssesAttention
 
         cpa = UlyssesAttention(scenario(world)["workload"]["mask"], HQ, HK, D)
-    elif mode == "capi":
+    elif mode in ("capi", "capi_p2p"):
         from paper_2505_13211_b200.cp import CPExecutorC
 
-        cpa = CPExecutorC(scenario(world), HQ, HK, D)
+        cpa = CPExecutorC(scenario(world), HQ, HK, D, transport="p2p" if mode == "capi_p2p" else "nccl")
     else:
         cpa = CPAttention(scenario(world), HQ, HK, D, transport="p2p" if mode == "p2p" else "nccl")
     L = cpa.local_tokens
@@ -261,6 +261,11 @@ def run(args) -> None:
             # host fwd + per stage (gather x2, ffa), cast; preprocess, host bwd (2), per stage
             # (gather x2, dkdv, dq, scatter-adds), final casts
             n_launch = 2 + 3 * nf + 1 + 3 + 4 * nb + 2 * world * nb + 3
+        elif mode == "capi_p2p":
+            nf, nb = cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"]
+            # fwd per stage: cast (wait, 2 copies, signal), wait, ffa, signal; bwd per stage: cast,
+            # 2 waits, dkdv + dq, 2 signals, reduce (wait, 2 scatter-adds per consumer, signal)
+            n_launch = 2 + 7 * nf + 1 + 3 + (4 + 6 + 2 + 2 * (world - 1)) * nb + 3
         else:
             for st in cpa.fwd_stages:
                 # p2p: flag wait + 2 copies + signal on the comm stream, wait + signal beside the FFA

@@ -12,6 +12,15 @@
 // other) + one scatter-add per source rank in rank order
 // (deterministic). Communication runs on two high-priority streams.
 //
+// Transport MAGIPLAN_CP_P2P (magiplan_cp_create_ex) moves the same bytes
+// over NVLink peer memory instead, as cp.py's transport="p2p" does: every
+// stage's receive buffers (and, backward, the partial dK / dV buffers) live
+// in IPC-exportable memory whose handles are all-gathered once at creation;
+// the GroupCast is one fused gather-and-send kernel writing straight into
+// the consumers' buffers, the GroupReduce one scatter-add per consumer (rank
+// order) reading its partials over NVLink, and stream-side release / acquire
+// flags order producers, consumers and buffer reuse across passes.
+//
 // NCCL is resolved at run time (dlopen of libnccl.so.2): the planner and
 // the kernels of this library do not depend on it.
 #include <cuda_runtime.h>
@@ -44,6 +53,16 @@ cudaError_t launch_range_scatter_add_f32(const float* src, float* dst, const int
                                          const int64_t* offsets, int64_t num_ranges, int64_t total_rows,
                                          int64_t row_elems, cudaStream_t stream);
 cudaError_t launch_cast_f32_bf16(const float* src, void* dst, int64_t n, cudaStream_t stream);
+cudaError_t launch_range_copy_to(const void* src, const int64_t* ranges, const int64_t* offsets,
+                                 const unsigned long long* dst_base, const int64_t* dst_row, int64_t num_ranges,
+                                 int64_t total_rows, int64_t row_bytes, cudaStream_t stream);
+cudaError_t launch_range_scatter_add_from(float* dst, const int64_t* ranges, const int64_t* offsets,
+                                          const unsigned long long* src_base, const int64_t* src_row,
+                                          int64_t num_ranges, int64_t total_rows, int64_t row_elems,
+                                          cudaStream_t stream);
+cudaError_t launch_flags_signal(unsigned int* const* flags, int n, unsigned int value, cudaStream_t stream);
+cudaError_t launch_flags_wait(const unsigned int* flags, unsigned int mask, unsigned int value,
+                              cudaStream_t stream);
 }  // namespace magi
 
 struct magiplan_ffa_plan {
@@ -87,6 +106,7 @@ struct Nccl {
   int (*GroupEnd)() = nullptr;
   int (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   int (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
 };
 
@@ -110,9 +130,10 @@ const Nccl& nccl() {
     lib.GroupEnd = reinterpret_cast<decltype(lib.GroupEnd)>(sym("ncclGroupEnd"));
     lib.Send = reinterpret_cast<decltype(lib.Send)>(sym("ncclSend"));
     lib.Recv = reinterpret_cast<decltype(lib.Recv)>(sym("ncclRecv"));
+    lib.AllGather = reinterpret_cast<decltype(lib.AllGather)>(sym("ncclAllGather"));
     lib.GetErrorString = reinterpret_cast<decltype(lib.GetErrorString)>(sym("ncclGetErrorString"));
     if (!lib.GetUniqueId || !lib.CommInitRank || !lib.CommSplit || !lib.Send || !lib.Recv || !lib.GroupStart ||
-        !lib.GroupEnd)
+        !lib.GroupEnd || !lib.AllGather)
       error = "NCCL library lacks the point-to-point / split API (needs NCCL >= 2.18)";
   });
   if (!error.empty()) throw DeviceError(error);
@@ -134,6 +155,22 @@ T* device_copy(const std::vector<T>& host) {
   cuda_check(cudaMemcpy(p, host.data(), host.size() * sizeof(T), cudaMemcpyHostToDevice), "cp executor upload");
   return static_cast<T*>(p);
 }
+
+// owning device copy of a host array (nullptr when empty)
+template <typename T>
+struct DevArr {
+  T* p = nullptr;
+  DevArr() = default;
+  explicit DevArr(const std::vector<T>& host) : p(device_copy(host)) {}
+  DevArr(DevArr&& o) noexcept : p(o.p) { o.p = nullptr; }
+  DevArr& operator=(DevArr&& o) noexcept {
+    std::swap(p, o.p);
+    return *this;
+  }
+  DevArr(const DevArr&) = delete;
+  DevArr& operator=(const DevArr&) = delete;
+  ~DevArr() { cudaFree(p); }
+};
 
 // ---------------------------------------------------------------- plan view
 struct RangeList {  // ranges of local rows + packed offsets, on the device
@@ -169,6 +206,28 @@ struct Stage {
   std::unique_ptr<magiplan_ffa_plan> plan;
 };
 
+// One stage over peer memory. Flag block (uint32, index = peer rank), each
+// entry written by that peer into this rank's block: [ready | consumed |
+// partials ready | partials read].
+struct PeerStage {
+  void *kb = nullptr, *vb = nullptr;     // this rank's receive buffers (bf16)
+  float *dkb = nullptr, *dvb = nullptr;  // this rank's partial dK / dV (backward)
+  uint32_t* flags = nullptr;
+  // GroupCast as producer: every consumer's receive entries from this rank
+  int64_t n = 0, rows = 0;
+  DevArr<int64_t> ranges, offs, drow;
+  DevArr<uint64_t> kbase, vbase;
+  DevArr<uint64_t> sig_send, sig_recv, sig_pready, sig_pdone;
+  int n_dest = 0, n_src = 0;
+  uint32_t mask_dest = 0, mask_src = 0;
+  struct Dst {  // GroupReduce as owner: one consumer's partial rows of this rank's keys
+    int64_t n = 0, rows = 0;
+    DevArr<int64_t> ranges, offs, row;
+    DevArr<uint64_t> bdk, bdv;
+  };
+  std::vector<Dst> per_dst;  // consumers in rank order
+};
+
 std::unique_ptr<magiplan_ffa_plan> make_ffa_plan(const json& slices, int64_t sq, int64_t sk, int32_t d,
                                                  bool always = false) {
   if (slices.empty() && !always) return nullptr;
@@ -198,10 +257,18 @@ struct CpExecutor {
   std::vector<Stage> fwd, bwd;
   ncclComm_t cast_comm = nullptr, reduce_comm = nullptr;
   cudaStream_t comm_stream = nullptr, reduce_stream = nullptr;
+  // peer-memory transport
+  bool p2p = false;
+  std::vector<PeerStage> pfwd, pbwd;
+  std::vector<void*> owned, opened;
+  uint32_t epoch = 0, bepoch = 0;
 
   ~CpExecutor() {
     if (comm_stream) cudaStreamSynchronize(comm_stream);
     if (reduce_stream) cudaStreamSynchronize(reduce_stream);
+    if (p2p) cudaDeviceSynchronize();
+    for (void* p : opened) cudaIpcCloseMemHandle(p);
+    for (void* p : owned) cudaFree(p);
     if (cast_comm) nccl().CommDestroy(cast_comm);
     if (reduce_comm) nccl().CommDestroy(reduce_comm);
     if (comm_stream) cudaStreamDestroy(comm_stream);
@@ -227,6 +294,194 @@ struct CpExecutor {
       ro += rb;
     }
     nccl_check(n.GroupEnd(), "ncclGroupEnd");
+  }
+
+  void* ipc_alloc(size_t bytes, std::vector<cudaIpcMemHandle_t>& handles) {
+    void* p = nullptr;
+    cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "p2p alloc");
+    owned.push_back(p);
+    cudaIpcMemHandle_t h;
+    cuda_check(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+    handles.push_back(h);
+    return p;
+  }
+
+  // Receive / partial buffers and flags of every stage, handles all-gathered
+  // over the cast communicator, the peers' buffers mapped, and the device
+  // arrays of the fused kernels built from the executor plan.
+  void setup_p2p(const json& xp) {
+    if (world > 32) throw UsageError("p2p transport: at most 32 ranks (flag masks)");
+    const size_t krow = kv_row_bytes(), grow = grad_row_bytes();
+    std::vector<cudaIpcMemHandle_t> mine;
+    const std::pair<const char*, std::vector<Stage>*> passes[2] = {{"fwd_stages", &fwd}, {"bwd_stages", &bwd}};
+    for (const auto& [key, stages] : passes) {
+      const bool back = stages == &bwd;
+      auto& ps = back ? pbwd : pfwd;
+      ps.resize(stages->size());
+      for (size_t j = 0; j < stages->size(); ++j) {
+        PeerStage& P = ps[j];
+        const size_t bt = static_cast<size_t>((*stages)[j].buf_tokens);
+        P.kb = ipc_alloc(bt * krow, mine);
+        P.vb = ipc_alloc(bt * krow, mine);
+        if (back) {
+          P.dkb = static_cast<float*>(ipc_alloc(bt * grow, mine));
+          P.dvb = static_cast<float*>(ipc_alloc(bt * grow, mine));
+        }
+        P.flags = static_cast<uint32_t*>(ipc_alloc(16 * static_cast<size_t>(world), mine));
+        cuda_check(cudaMemset(P.flags, 0, 16 * static_cast<size_t>(world)), "p2p flags");
+      }
+    }
+    // all-gather the handles (the flags are zero everywhere before any peer can signal)
+    const size_t hb = mine.size() * sizeof(cudaIpcMemHandle_t);
+    void *d_send = nullptr, *d_all = nullptr;
+    cuda_check(cudaMalloc(&d_send, std::max<size_t>(hb, 16)), "p2p handles");
+    cuda_check(cudaMalloc(&d_all, std::max<size_t>(hb * world, 16)), "p2p handles");
+    cuda_check(cudaMemcpy(d_send, mine.data(), hb, cudaMemcpyHostToDevice), "p2p handles");
+    cuda_check(cudaDeviceSynchronize(), "p2p handles");
+    nccl_check(nccl().AllGather(d_send, d_all, hb, kNcclInt8, cast_comm, comm_stream), "ncclAllGather");
+    std::vector<cudaIpcMemHandle_t> all(mine.size() * static_cast<size_t>(world));
+    cuda_check(cudaStreamSynchronize(comm_stream), "p2p handles");
+    cuda_check(cudaMemcpy(all.data(), d_all, hb * world, cudaMemcpyDeviceToHost), "p2p handles");
+    cudaFree(d_send);
+    cudaFree(d_all);
+
+    const json& ranks = xp["ranks"];
+    size_t hidx = 0;  // handle index of the stage's first buffer, same on every rank
+    for (const auto& [key, stages] : passes) {
+      const bool back = stages == &bwd;
+      const size_t per = back ? 5 : 3;  // k, v, (dk, dv,) flags
+      auto& ps = back ? pbwd : pfwd;
+      for (size_t j = 0; j < stages->size(); ++j, hidx += per) {
+        PeerStage& P = ps[j];
+        std::vector<std::vector<uint64_t>> peer(static_cast<size_t>(world));
+        for (int d = 0; d < world; ++d) {
+          if (d == rank) continue;
+          for (size_t b = 0; b < per; ++b) {
+            void* o = nullptr;
+            cuda_check(cudaIpcOpenMemHandle(&o, all[static_cast<size_t>(d) * mine.size() + hidx + b],
+                                            cudaIpcMemLazyEnablePeerAccess),
+                       "cudaIpcOpenMemHandle");
+            opened.push_back(o);
+            peer[static_cast<size_t>(d)].push_back(reinterpret_cast<uint64_t>(o));
+          }
+        }
+        auto flag_of = [&](int d, int block) {  // entry `rank` of block `block` in d's flags
+          return peer[static_cast<size_t>(d)][per - 1] + 4ull * (static_cast<uint64_t>(block) * world + rank);
+        };
+        std::vector<int64_t> ranges, offs, drow;
+        std::vector<uint64_t> kbase, vbase, sig_send, sig_pdone;
+        for (int d = 0; d < world; ++d) {
+          const json& other = ranks[static_cast<size_t>(d)][key];
+          if (d == rank || j >= other.size()) continue;
+          PeerStage::Dst dst;
+          std::vector<int64_t> rr, ro, rrow;
+          std::vector<uint64_t> bdk, bdv;
+          bool any = false;
+          for (const auto& e : other[j]["recv"]) {
+            if (e[0].get<int>() != rank) continue;
+            any = true;
+            const int64_t len = e[2].get<int64_t>() - e[1].get<int64_t>();
+            const int64_t src_local = e[3].get<int64_t>(), buf_off = e[4].get<int64_t>();
+            ranges.push_back(src_local);
+            ranges.push_back(src_local + len);
+            offs.push_back(P.rows);
+            P.rows += len;
+            kbase.push_back(peer[static_cast<size_t>(d)][0]);
+            vbase.push_back(peer[static_cast<size_t>(d)][1]);
+            drow.push_back(buf_off);
+            if (back) {
+              rr.push_back(src_local);
+              rr.push_back(src_local + len);
+              ro.push_back(dst.rows);
+              dst.rows += len;
+              bdk.push_back(peer[static_cast<size_t>(d)][2]);
+              bdv.push_back(peer[static_cast<size_t>(d)][3]);
+              rrow.push_back(buf_off);
+            }
+          }
+          if (!any) continue;
+          P.mask_dest |= 1u << d;
+          ++P.n_dest;
+          sig_send.push_back(flag_of(d, 0));
+          if (back) {
+            sig_pdone.push_back(flag_of(d, 3));
+            dst.n = static_cast<int64_t>(ro.size());
+            dst.ranges = DevArr<int64_t>(rr);
+            dst.offs = DevArr<int64_t>(ro);
+            dst.row = DevArr<int64_t>(rrow);
+            dst.bdk = DevArr<uint64_t>(bdk);
+            dst.bdv = DevArr<uint64_t>(bdv);
+            P.per_dst.push_back(std::move(dst));
+          }
+        }
+        P.n = static_cast<int64_t>(offs.size());
+        P.ranges = DevArr<int64_t>(ranges);
+        P.offs = DevArr<int64_t>(offs);
+        P.drow = DevArr<int64_t>(drow);
+        P.kbase = DevArr<uint64_t>(kbase);
+        P.vbase = DevArr<uint64_t>(vbase);
+        P.sig_send = DevArr<uint64_t>(sig_send);
+        P.sig_pdone = DevArr<uint64_t>(sig_pdone);
+        // as consumer: the sources of this stage's receive entries
+        std::vector<uint64_t> sig_recv, sig_pready;
+        const json& me = ranks[static_cast<size_t>(rank)][key];
+        if (j < me.size()) {
+          for (const auto& e : me[j]["recv"]) {
+            const int s_ = e[0].get<int>();
+            if (P.mask_src >> s_ & 1u) continue;
+            P.mask_src |= 1u << s_;
+          }
+          for (int s_ = 0; s_ < world; ++s_) {
+            if (!(P.mask_src >> s_ & 1u)) continue;
+            ++P.n_src;
+            sig_recv.push_back(flag_of(s_, 1));
+            if (back) sig_pready.push_back(flag_of(s_, 2));
+          }
+        }
+        P.sig_recv = DevArr<uint64_t>(sig_recv);
+        P.sig_pready = DevArr<uint64_t>(sig_pready);
+      }
+    }
+    p2p = true;
+  }
+
+  void flags_wait(const PeerStage& P, int block, uint32_t mask, uint32_t value, cudaStream_t s) const {
+    cuda_check(magi::launch_flags_wait(P.flags + static_cast<size_t>(block) * world, mask, value, s),
+               "flags_wait launch");
+  }
+  static void flags_signal(const DevArr<uint64_t>& ptrs, int n, uint32_t value, cudaStream_t s) {
+    cuda_check(magi::launch_flags_signal(reinterpret_cast<unsigned int* const*>(ptrs.p), n, value, s),
+               "flags_signal launch");
+  }
+
+  // GroupCast of one stage over peer memory on the comm stream: wait until
+  // every consumer released the buffer of the previous pass, copy the ranges
+  // into the consumers' buffers, raise their ready flags
+  void cast_p2p(const PeerStage& P, uint32_t ep, const void* k, const void* v) const {
+    flags_wait(P, 1, P.mask_dest, ep - 1, comm_stream);
+    if (P.n) {
+      for (const auto& [src, base] : {std::pair<const void*, const uint64_t*>{k, P.kbase.p}, {v, P.vbase.p}})
+        cuda_check(magi::launch_range_copy_to(src, P.ranges.p, P.offs.p,
+                                              reinterpret_cast<const unsigned long long*>(base), P.drow.p, P.n,
+                                              P.rows, static_cast<int64_t>(kv_row_bytes()), comm_stream),
+                   "range_copy_to launch");
+    }
+    flags_signal(P.sig_send, P.n_dest, ep, comm_stream);
+  }
+
+  // GroupReduce of one backward stage over peer memory on the reduce stream:
+  // the consumers' partials, per consumer in rank order, added into dk / dv
+  void reduce_p2p(const PeerStage& P, uint32_t ep, float* dk32, float* dv32) const {
+    flags_wait(P, 2, P.mask_dest, ep, reduce_stream);
+    for (const auto& dst : P.per_dst) {
+      if (!dst.n) continue;
+      for (const auto& [acc, base] : {std::pair<float*, const uint64_t*>{dk32, dst.bdk.p}, {dv32, dst.bdv.p}})
+        cuda_check(magi::launch_range_scatter_add_from(acc, dst.ranges.p, dst.offs.p,
+                                                       reinterpret_cast<const unsigned long long*>(base),
+                                                       dst.row.p, dst.n, dst.rows, hk * d, reduce_stream),
+                   "range_scatter_add_from launch");
+    }
+    flags_signal(P.sig_pdone, P.n_dest, ep, reduce_stream);
   }
 
   struct Cast {
@@ -310,10 +565,19 @@ magiplan_status magiplan_cp_unique_id(void* out_id) {
 magiplan_status magiplan_cp_create(const magiplan_scenario* scenario, int32_t rank, const void* nccl_unique_id,
                                    int64_t num_heads_q, int64_t num_heads_k, int32_t head_dim, float softmax_scale,
                                    magiplan_cp** out) {
+  return magiplan_cp_create_ex(scenario, rank, nccl_unique_id, num_heads_q, num_heads_k, head_dim, softmax_scale,
+                               MAGIPLAN_CP_NCCL, out);
+}
+
+magiplan_status magiplan_cp_create_ex(const magiplan_scenario* scenario, int32_t rank, const void* nccl_unique_id,
+                                      int64_t num_heads_q, int64_t num_heads_k, int32_t head_dim,
+                                      float softmax_scale, int32_t transport, magiplan_cp** out) {
   MAGI_REQUIRE(scenario && nccl_unique_id && out);
   auto* cp = new magiplan_cp;
   const magiplan_status st = guarded([&] {
     using namespace magiplan;
+    if (transport != MAGIPLAN_CP_NCCL && transport != MAGIPLAN_CP_P2P)
+      throw UsageError("transport must be MAGIPLAN_CP_NCCL or MAGIPLAN_CP_P2P");
     if (num_heads_q <= 0 || num_heads_k <= 0 || num_heads_q % num_heads_k != 0)
       throw UsageError("num_heads_q must be a positive multiple of num_heads_k");
     if (head_dim != 64 && head_dim != 128) throw UsageError("head_dim must be 64 or 128");
@@ -380,6 +644,7 @@ magiplan_status magiplan_cp_create(const magiplan_scenario* scenario, int32_t ra
     // the cast communicator from the id, the reduce communicator split off it
     nccl_check(n.CommInitRank(&ex.cast_comm, ex.world, id, rank), "ncclCommInitRank");
     nccl_check(n.CommSplit(ex.cast_comm, 0, rank, &ex.reduce_comm, nullptr), "ncclCommSplit");
+    if (transport == MAGIPLAN_CP_P2P && ex.world > 1) ex.setup_p2p(xp);
     json dj;
     dj["rank"] = rank;
     dj["cp_size"] = ex.world;
@@ -389,6 +654,7 @@ magiplan_status magiplan_cp_create(const magiplan_scenario* scenario, int32_t ra
     dj["num_stages_fwd"] = xp["num_stages_fwd"];
     dj["num_stages_bwd"] = xp["num_stages_bwd"];
     dj["area_multiplicity"] = xp["area_multiplicity"];
+    dj["transport"] = ex.p2p ? "p2p" : "nccl";
     ex.describe = dj.dump();
   });
   if (st != MAGIPLAN_OK) {
@@ -417,7 +683,15 @@ magiplan_status magiplan_cp_forward(magiplan_cp* cp, const void* q, const void* 
     const int hq = static_cast<int>(ex.hq), hk = static_cast<int>(ex.hk);
     wait_and_destroy(ex.comm_stream, record(cur));
     std::vector<CpExecutor::Cast> casts;
-    if (!ex.fwd.empty()) casts.push_back(ex.cast(ex.fwd[0], k, v));
+    const bool p2p = ex.p2p;
+    const uint32_t ep = p2p ? ++ex.epoch : 0;
+    auto cast = [&](size_t j) {
+      if (p2p)
+        ex.cast_p2p(ex.pfwd[j], ep, k, v);
+      else
+        casts.push_back(ex.cast(ex.fwd[j], k, v));
+    };
+    if (!ex.fwd.empty()) cast(0);
     auto ffa = [&](const magiplan_ffa_plan* pl, const void* kk, const void* vv, int acc) {
       const FfaPlan& P = pl->plan;
       cuda_check(magi::launch_ffa_fwd(magiplan::fwd_work(P),
@@ -428,9 +702,18 @@ magiplan_status magiplan_cp_forward(magiplan_cp* cp, const void* q, const void* 
     ffa(ex.host_plan.get(), k, v, 0);
     for (size_t j = 0; j < ex.fwd.size(); ++j) {
       // cast(j+1) is issued before FFA(j) consumes cast(j)
-      if (j + 1 < ex.fwd.size()) casts.push_back(ex.cast(ex.fwd[j + 1], k, v));
-      cuda_check(cudaStreamWaitEvent(cur, casts[j].done, 0), "cp wait cast");
-      if (ex.fwd[j].plan) ffa(ex.fwd[j].plan.get(), casts[j].k, casts[j].v, 1);
+      if (j + 1 < ex.fwd.size()) cast(j + 1);
+      if (p2p) {
+        // the producers' copies into this rank's buffers have landed
+        const PeerStage& P = ex.pfwd[j];
+        ex.flags_wait(P, 0, P.mask_src, ep, cur);
+        if (ex.fwd[j].plan) ffa(ex.fwd[j].plan.get(), P.kb, P.vb, 1);
+        // release the buffers: the producers may overwrite them next pass
+        CpExecutor::flags_signal(P.sig_recv, P.n_src, ep, cur);
+      } else {
+        cuda_check(cudaStreamWaitEvent(cur, casts[j].done, 0), "cp wait cast");
+        if (ex.fwd[j].plan) ffa(ex.fwd[j].plan.get(), casts[j].k, casts[j].v, 1);
+      }
     }
     if (out_bf16)
       cuda_check(magi::launch_cast_f32_bf16(out_f32, out_bf16, L * ex.hq * ex.d, cur), "cast launch");
@@ -455,7 +738,15 @@ magiplan_status magiplan_cp_backward(magiplan_cp* cp, const void* q, const void*
     cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&dv32), std::max<size_t>(gk * 4, 16), cur), "alloc");
     wait_and_destroy(ex.comm_stream, record(cur));
     std::vector<CpExecutor::Cast> casts;
-    if (!ex.bwd.empty()) casts.push_back(ex.cast(ex.bwd[0], k, v));
+    const bool p2p = ex.p2p;
+    const uint32_t eb = p2p ? ++ex.bepoch : 0;
+    auto cast = [&](size_t j) {
+      if (p2p)
+        ex.cast_p2p(ex.pbwd[j], eb, k, v);
+      else
+        casts.push_back(ex.cast(ex.bwd[j], k, v));
+    };
+    if (!ex.bwd.empty()) cast(0);
     cuda_check(magi::launch_ffa_bwd_preprocess(out_f32, dout, delta, L, hq, static_cast<int>(d), 1, cur),
                "preprocess launch");
     {
@@ -469,21 +760,46 @@ magiplan_status magiplan_cp_backward(magiplan_cp* cp, const void* q, const void*
     const size_t grb = ex.grad_row_bytes();
     for (size_t j = 0; j < ex.bwd.size(); ++j) {
       const Stage& st = ex.bwd[j];
-      if (j + 1 < ex.bwd.size()) casts.push_back(ex.cast(ex.bwd[j + 1], k, v));
-      cuda_check(cudaStreamWaitEvent(cur, casts[j].done, 0), "cp wait cast");
+      if (j + 1 < ex.bwd.size()) cast(j + 1);
       // the stage's partial dK / dV (written whole by the pass) and dQ += ...
       float *pk = nullptr, *pv = nullptr;
-      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&pk), std::max<size_t>(st.buf_tokens * grb, 16), cur),
-                 "alloc");
-      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&pv), std::max<size_t>(st.buf_tokens * grb, 16), cur),
-                 "alloc");
+      const void *kk = nullptr, *vv = nullptr;
+      if (p2p) {
+        // the producers' K / V have landed, and the owners have read last
+        // pass's partials out of this rank's partial buffers
+        const PeerStage& P = ex.pbwd[j];
+        ex.flags_wait(P, 0, P.mask_src, eb, cur);
+        ex.flags_wait(P, 3, P.mask_src, eb - 1, cur);
+        pk = P.dkb;
+        pv = P.dvb;
+        kk = P.kb;
+        vv = P.vb;
+      } else {
+        cuda_check(cudaStreamWaitEvent(cur, casts[j].done, 0), "cp wait cast");
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&pk), std::max<size_t>(st.buf_tokens * grb, 16), cur),
+                   "alloc");
+        cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&pv), std::max<size_t>(st.buf_tokens * grb, 16), cur),
+                   "alloc");
+        kk = casts[j].k;
+        vv = casts[j].v;
+      }
       if (st.plan) {
-        const magiplan_status s = magiplan_ffa_bwd_stage(st.plan.get(), q, casts[j].k, casts[j].v, lse, delta,
-                                                         dout, dq32, pk, pv, hq, hk, ex.scale, cur);
+        const magiplan_status s = magiplan_ffa_bwd_stage(st.plan.get(), q, kk, vv, lse, delta, dout, dq32, pk, pv,
+                                                         hq, hk, ex.scale, cur);
         if (s != MAGIPLAN_OK) throw DeviceError(magiplan_last_error());
       } else if (st.buf_tokens) {
         cuda_check(cudaMemsetAsync(pk, 0, st.buf_tokens * grb, cur), "memset");
         cuda_check(cudaMemsetAsync(pv, 0, st.buf_tokens * grb, cur), "memset");
+      }
+      if (p2p) {
+        // release this stage's K / V buffers, publish the partials; the
+        // owners add them in on their reduce streams
+        const PeerStage& P = ex.pbwd[j];
+        CpExecutor::flags_signal(P.sig_recv, P.n_src, eb, cur);
+        CpExecutor::flags_signal(P.sig_pready, P.n_src, eb, cur);
+        wait_and_destroy(ex.reduce_stream, record(cur));
+        ex.reduce_p2p(P, eb, dk32, dv32);
+        continue;
       }
       // GroupReduce(j) on its own stream and communicator, under FFA(j+1)
       wait_and_destroy(ex.reduce_stream, record(cur));

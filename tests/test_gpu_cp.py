@@ -82,10 +82,12 @@ def _worker(rank, world, port, mask, chunk, hq, hk, d, outq, mode, stages, check
         elif mode == "ring":
             cpa = RingAttention(mask, hq, hk, d)
             S = cpa.chunk_size * 2 * world
-        elif mode == "capi":  # the C-ABI executor (csrc/host/cp_exec.cpp)
+        elif mode in ("capi", "capi_p2p"):  # the C-ABI executor (csrc/host/cp_exec.cpp)
             from paper_2505_13211_b200.cp import CPExecutorC
 
-            cpa = CPExecutorC(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d)
+            cpa = CPExecutorC(_scenario(mask, world, chunk, hq, hk, d, stages), hq, hk, d,
+                              transport="p2p" if mode == "capi_p2p" else "nccl")
+            assert cpa.transport == ("p2p" if mode == "capi_p2p" else "nccl")
             S = cpa.xplan["seqlen"]
             nst = (cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"])
         else:
@@ -189,6 +191,11 @@ CASES = [
     ("capi", BC4096, 256, 3),
     ("capi", VARLEN, 128, 4),
     ("capi", CAUSAL, 192, None),
+    # the C-ABI executor over NVLink peer memory (fused gather-and-send,
+    # scatter-add reading the consumers' partials, stream-side flags)
+    ("capi_p2p", BC4096, 256, 3),
+    ("capi_p2p", VARLEN, 128, 4),
+    ("capi_p2p", CAUSAL, 192, None),
     # the forward GroupCast over NVLink peer memory (IPC-mapped receive
     # buffers, one range-copy kernel, stream-side flags) instead of NCCL
     ("p2p", BC4096, 256, 3),
@@ -212,7 +219,7 @@ def test_cp_matches_oracle(built_lib, cuda, world, mode, mask, chunk, stages):
 
 
 def _check_vs_oracle(world, mode, mask, chunk, stages):
-    if torch.cuda.device_count() < world and mode in ("capi", "p2p"):
+    if torch.cuda.device_count() < world and mode in ("capi", "capi_p2p", "p2p"):
         pytest.skip(f"{mode}: one rank per GPU, needs {world} GPUs")
     from oracle import oracle
     from paper_2505_13211_b200.planner import Mask
