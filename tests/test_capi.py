@@ -158,6 +158,25 @@ def test_ffa_plan_validation_on_cpu(built_lib):
     assert st == _lib.ERR_USAGE and b"head_dim" in L.magiplan_last_error()
 
 
+def test_cp_create_argument_validation_on_cpu(built_lib):
+    """The CP executor rejects a bad transport / head layout before touching
+    CUDA or NCCL (USAGE error, handle untouched)."""
+    from paper_2505_13211_b200 import _lib
+    from paper_2505_13211_b200.planner import Scenario
+
+    L = built_lib
+    sc = Scenario({"workload": {"mask": {"seqlen": 4096, "pattern": "causal"}, "num_heads_q": 4,
+                                "num_heads_k": 2, "head_dim": 128}, "cp_size": 2})
+    uid = C.create_string_buffer(128)
+    h = C.c_void_p()
+    st = L.magiplan_cp_create_ex(sc._h, 0, uid, 4, 2, 128, 0.088, 7, C.byref(h))
+    assert st == _lib.ERR_USAGE and b"transport" in L.magiplan_last_error() and h.value is None
+    st = L.magiplan_cp_create_ex(sc._h, 0, uid, 4, 3, 128, 0.088, 1, C.byref(h))
+    assert st == _lib.ERR_USAGE and b"multiple of num_heads_k" in L.magiplan_last_error()
+    st = L.magiplan_cp_create_ex(sc._h, 0, uid, 4, 2, 96, 0.088, 0, C.byref(h))
+    assert st == _lib.ERR_USAGE and b"head_dim" in L.magiplan_last_error()
+
+
 # ---------------------------------------------------------------- a plain C consumer
 def _build_c_consumer() -> Path:
     """gcc-compile tests/c_consumer/ffa_consumer.c against include/ and the
