@@ -301,7 +301,10 @@ class CPAttention:
         _lib.check(self.L.magiplan_flags_signal(ptrs.data_ptr(), n, value, stream.cuda_stream))
 
     def close(self):
-        """Release the peer-memory mappings and buffers (p2p transport)."""
+        """Release the peer-memory mappings and buffers (p2p transport).
+        Safe once this rank's passes have completed: a backward pass ends only
+        after the owners have read its partials, and peers write into this
+        rank's receive buffers only inside passes it takes part in."""
         if not self._p2p_owned and not self._p2p_opened:
             return
         torch.cuda.synchronize(self.device)
@@ -585,6 +588,12 @@ class CPAttention:
             if not p2p:
                 keep.append((kb, vb, sent, dkb, dvb, recv))
         cur.wait_stream(self.reduce_stream)
+        if p2p:
+            # the owners have read this pass's partials out of this rank's
+            # buffers: once the pass completes, no peer touches them (so the
+            # buffers may be freed after a stream synchronize)
+            for P in self._p2p_bwd:
+                self._flags_wait(P, 3, P["mask_src"], eb, cur)
         outs = []
         for t in (dq, dk, dv):
             b = torch.empty(t.shape, dtype=torch.bfloat16, device=dev)

@@ -265,7 +265,8 @@ def run(args) -> None:
             nf, nb = cpa.xplan["num_stages_fwd"], cpa.xplan["num_stages_bwd"]
             # fwd per stage: cast (wait, 2 copies, signal), wait, ffa, signal; bwd per stage: cast,
             # 2 waits, dkdv + dq, 2 signals, reduce (wait, 2 scatter-adds per consumer, signal)
-            n_launch = 2 + 7 * nf + 1 + 3 + (4 + 6 + 2 + 2 * (world - 1)) * nb + 3
+            # (+ the end-of-pass wait on the owners' reads), final casts
+            n_launch = 2 + 7 * nf + 1 + 3 + (4 + 6 + 2 + 2 * (world - 1) + 1) * nb + 3
         else:
             for st in cpa.fwd_stages:
                 # p2p: flag wait + 2 copies + signal on the comm stream, wait + signal beside the FFA
@@ -273,8 +274,8 @@ def run(args) -> None:
             if mode == "p2p":
                 # per stage: cast (wait, 2 copies, signal), compute (2 waits, dK/dV + dQ, 2 signals),
                 # reduce (wait, 2 scatter-adds per consumer, signal)
-                for P in cpa._p2p_bwd:
-                    n_launch += 4 + 6 + 2 + 2 * len(P["per_dst"])
+                for P in cpa._p2p_bwd:  # (+ the end-of-pass wait on the owners' reads)
+                    n_launch += 4 + 6 + 2 + 2 * len(P["per_dst"]) + 1
             else:
                 for st in cpa.bwd_stages:
                     n_launch += 2 + 2 * (1 if sum(st.send_splits) else 0) + 2 * world

@@ -834,6 +834,11 @@ magiplan_status magiplan_cp_backward(magiplan_cp* cp, const void* q, const void*
       recvs.push_back(rv);
     }
     wait_and_destroy(cur, record(ex.reduce_stream));
+    if (p2p) {
+      // the owners have read this pass's partials: once the pass completes
+      // no peer touches this rank's buffers (magiplan_cp_free needs no barrier)
+      for (const PeerStage& P : ex.pbwd) ex.flags_wait(P, 3, P.mask_src, eb, cur);
+    }
     cuda_check(magi::launch_cast_f32_bf16(dq32, dq, static_cast<int64_t>(gq), cur), "cast launch");
     cuda_check(magi::launch_cast_f32_bf16(dk32, dk, static_cast<int64_t>(gk), cur), "cast launch");
     cuda_check(magi::launch_cast_f32_bf16(dv32, dv, static_cast<int64_t>(gk), cur), "cast launch");
