@@ -314,6 +314,12 @@ class CPAttention:
             self.L.magiplan_p2p_free(ptr)
         self._p2p_opened, self._p2p_owned, self._p2p, self._p2p_bwd = [], [], [], []
 
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown / CUDA already torn down
+            pass
+
     def _cast_p2p(self, P: dict, epoch: int, k: torch.Tensor, v: torch.Tensor):
         """GroupCast of one stage over peer memory, on the comm stream: wait
         until every consumer has released this stage's buffer from the
