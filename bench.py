@@ -155,6 +155,43 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+class EnergyMeter:
+    """NVML's total-energy counter (mJ) read on both sides of the timed
+    region: joules per step and mean board power under the power cap. None
+    when NVML is unavailable; it never fails the bench."""
+
+    def __init__(self, gpu: int):
+        self.h = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+        except Exception:  # noqa: BLE001
+            self.h = None
+        self.e0 = self.t0 = None
+
+    def _read(self):
+        if self.h is None:
+            return None
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h))
+        except Exception:  # noqa: BLE001
+            return None
+
+    def start(self):
+        self.e0, self.t0 = self._read(), time.perf_counter()
+
+    def stop(self, steps: int) -> dict | None:
+        e1, t1 = self._read(), time.perf_counter()
+        if self.e0 is None or e1 is None or e1 <= self.e0 or steps <= 0:
+            return None
+        joules = (e1 - self.e0) * 1e-3
+        return {"j_per_step": joules / steps, "avg_w": joules / (t1 - self.t0),
+                "source": "NVML total energy counter around the timed region (host-clocked)"}
+
+
 def cpu_baseline_sample(wl: dict, target_s: float = 12.0) -> dict:
     """Oracle port (oracle/ffa_oracle.c) fwd (f32 accumulate) + bwd on a bounded
     sample of the workload: the first `rows` query rows of chunk 0 against its
@@ -366,7 +403,9 @@ def run_single(args) -> None:
           for _ in range(args.steps)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
+    energy = EnergyMeter(0)
     torch.cuda.synchronize()
+    energy.start()
     start.record(stream)
     for s in range(args.steps):
         ev[s][0].record(stream)
@@ -375,6 +414,7 @@ def run_single(args) -> None:
             ev[s][i + 1].record(stream)
     end.record(stream)
     torch.cuda.synchronize()
+    step_energy = energy.stop(args.steps)
     total_ms = start.elapsed_time(end)
     per_part = {name: statistics.mean(ev[s][i].elapsed_time(ev[s][i + 1]) for s in range(args.steps))
                 for i, (name, _, _) in enumerate(parts)}
@@ -494,6 +534,7 @@ def run_single(args) -> None:
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
                 "copies": "H2D q, k, v, dO; D2H O, dQ, dK, dV (bf16), every step"},
         "clocks": clk,
+        "energy": step_energy,
         "gpu_launches": launches_per_step * args.steps,
     }
     del sets, q, k, v, do, out, dq, dk, dv
