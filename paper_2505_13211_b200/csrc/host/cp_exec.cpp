@@ -332,18 +332,21 @@ struct CpExecutor {
       }
     }
     // all-gather the handles (the flags are zero everywhere before any peer can signal)
+    // every rank has the same stage counts, hence the same handle count
     const size_t hb = mine.size() * sizeof(cudaIpcMemHandle_t);
-    void *d_send = nullptr, *d_all = nullptr;
-    cuda_check(cudaMalloc(&d_send, std::max<size_t>(hb, 16)), "p2p handles");
-    cuda_check(cudaMalloc(&d_all, std::max<size_t>(hb * world, 16)), "p2p handles");
-    cuda_check(cudaMemcpy(d_send, mine.data(), hb, cudaMemcpyHostToDevice), "p2p handles");
+    if (hb == 0) {
+      p2p = true;
+      return;
+    }
+    std::vector<uint8_t> mine_bytes(hb);
+    std::memcpy(mine_bytes.data(), mine.data(), hb);
+    const DevArr<uint8_t> d_send(mine_bytes);
+    const DevArr<uint8_t> d_all(std::vector<uint8_t>(hb * static_cast<size_t>(world)));
     cuda_check(cudaDeviceSynchronize(), "p2p handles");
-    nccl_check(nccl().AllGather(d_send, d_all, hb, kNcclInt8, cast_comm, comm_stream), "ncclAllGather");
+    nccl_check(nccl().AllGather(d_send.p, d_all.p, hb, kNcclInt8, cast_comm, comm_stream), "ncclAllGather");
     std::vector<cudaIpcMemHandle_t> all(mine.size() * static_cast<size_t>(world));
     cuda_check(cudaStreamSynchronize(comm_stream), "p2p handles");
-    cuda_check(cudaMemcpy(all.data(), d_all, hb * world, cudaMemcpyDeviceToHost), "p2p handles");
-    cudaFree(d_send);
-    cudaFree(d_all);
+    cuda_check(cudaMemcpy(all.data(), d_all.p, hb * world, cudaMemcpyDeviceToHost), "p2p handles");
 
     const json& ranks = xp["ranks"];
     size_t hidx = 0;  // handle index of the stage's first buffer, same on every rank
